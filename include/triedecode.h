@@ -1,0 +1,206 @@
+/*
+ * triedecode.h -- C ABI of libtriedecode.so, the B200 (sm_100a) hot path of trie-based
+ * parallel beam decoding (arXiv 2502.00085, "PAPER.md").
+ *
+ * Citations: "P:<n>" = /root/reference/PAPER.md line n (section / algorithm named),
+ * "S:<n>" = SPEC.md line n.  Readings of silent or ambiguous passages: DESIGN.md "Readings".
+ *
+ * CONVENTIONS (apply to every entry point)
+ *  - Pointers are DEVICE pointers unless the name ends in `_host`.
+ *  - Every call is asynchronous on the caller's cudaStream_t and performs no host
+ *    synchronisation, except trie_create / trie_read_hyps / trie_status (documented).
+ *  - Ownership: the caller owns every buffer (Q, K/V pools, outputs, the workspace and
+ *    the attention scratch).  The library never calls cudaMalloc; the handle is a small
+ *    host struct holding pointers into the caller's workspace.  trie_destroy frees only
+ *    that host struct.
+ *  - Errors: each call returns TRIE_OK (0) or a negative code; a human-readable detail
+ *    is available from trie_last_error() (thread-local).  Faults that can only be
+ *    detected on the device latch bits into a device status word (TRIE_ST_*), read with
+ *    trie_status().
+ *  - Threading: a handle is bound to one stream at a time and is not thread-safe;
+ *    distinct handles are independent ("distinct sessions may run in
+ *    parallel").
+ *
+ * DATA LAYOUT
+ *  - KV pool, per layer: [R][Hkv][capacity][D], kv_dtype elements, head-major so that a
+ *    tile of consecutive slots of one (request, KV head) is one contiguous region (one
+ *    TMA box).  Slot n of request r holds trie node n (the prompt occupies slots 0..t-1).
+ *    Rows at slots >= N must hold FINITE values (zero-initialise pools once).
+ *  - Q / attention output: [R][b_live][Hq][D] (the QKV GEMM's row layout).
+ *  - New K/V rows for rope_kv_append: [R][b_live][Hkv][D].
+ *  - Trie metadata (inside the workspace, trie_get_arrays): token/parent/depth int32
+ *    [R][capacity], beam_mask uint32 [R][capacity] (bit r of word n <=> node n is on
+ *    the root-to-leaf path of beam r, generated nodes only), leaf int32 [R][32],
+ *    score float [R][32], n_nodes int32 [R], prompt_len int32 [R].
+ *    Invariants kept by the library: parent[n] < n; depth[] non-decreasing in slot
+ *    order; the b_live leaves are the last b_live slots after every append.
+ */
+#ifndef TRIEDECODE_H
+#define TRIEDECODE_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define TRIE_OK 0
+#define TRIE_EINVAL (-1)    /* bad shape or argument */
+#define TRIE_ESTATE (-2)    /* call-order violation (e.g. prune before any append) */
+#define TRIE_ECUDA (-3)     /* CUDA launch / runtime failure (detail in trie_last_error) */
+#define TRIE_ECAPACITY (-4) /* workspace or scratch too small */
+
+/* device status bits (latched; trie_status) */
+#define TRIE_ST_CAPACITY 0x1u    /* an append would exceed `capacity` slots */
+#define TRIE_ST_PARENT 0x2u      /* broken parent chain: parent[n] >= n or out of range */
+#define TRIE_ST_EMPTY_ROW 0x4u   /* attention row with no allowed key */
+#define TRIE_ST_LEAF 0x8u        /* leaf id outside [0, N) */
+
+/* kv_dtype */
+#define TRIE_F32 0
+#define TRIE_BF16 1
+
+typedef struct trie_cfg {
+  int32_t n_requests;     /* R: independent requests on this GPU (the data-parallel unit, §8(e)) */
+  int32_t beam_width;     /* b: 1..32 (b <= vocab)                                         */
+  int32_t max_prompt_len; /* t_max: row stride of the prompt token matrix                  */
+  int32_t capacity;       /* slots per request (>= t_max + b * steps without GC)           */
+  int32_t n_layers;       /* L                                                             */
+  int32_t n_q_heads;      /* Hq (local to this GPU)                                        */
+  int32_t n_kv_heads;     /* Hkv (local); Hq % Hkv == 0 (GQA)                       */
+  int32_t head_dim;       /* D: multiple of 16, <= 256                                     */
+  int32_t vocab;          /* V                                                             */
+  int32_t window;         /* W: sliding window in keys incl. self along the branch; 0 = dense */
+  int32_t gc_interval;    /* g: informational (the caller schedules trie_prune_compact)    */
+  int32_t kv_dtype;       /* TRIE_F32 or TRIE_BF16 (also the dtype of Q, new K/V, output)  */
+} trie_cfg;
+
+typedef struct trie_handle trie_handle;
+
+/* device pointers into the workspace, for passing to the pure entry points */
+typedef struct trie_arrays {
+  int32_t* token;
+  int32_t* parent;
+  int32_t* depth;
+  uint32_t* beam_mask;
+  int32_t* leaf;
+  float* score;
+  int32_t* n_nodes;
+  int32_t* prompt_len;
+  uint32_t* status;
+  int32_t b_live; /* live beams: 1 before the first append, then b (host-tracked) */
+  int32_t steps;  /* appends done since create/reset (host-tracked) */
+} trie_arrays;
+
+/* Workspace bytes for a configuration (metadata + scratch of beam_step / prune). */
+int trie_workspace_bytes(const trie_cfg* cfg, size_t* bytes);
+
+/*
+ * Alg. 2 l.1 initialize_trie(prompt): for every request r the prompt
+ * becomes a chain: token[i] = prompt[r][i], parent[i] = i-1 (-1 for i = 0), depth[i] = i
+ * (§3.4 positions), leaf = [t_r - 1], score = [0], N = t_r.
+ * prompt_lens_host [R] (host): 1 <= t_r <= t_max (EINVAL otherwise: empty prompt).
+ * prompt_tokens [R][t_max] int32 (device), copied into the workspace (trie_reset reuses it).
+ * Synchronises the stream once (validation of sizes).  Prompt K/V are the caller's
+ * (prefill is model context, not part of this library).
+ */
+int trie_create(const trie_cfg* cfg, void* workspace, size_t workspace_bytes,
+                const int32_t* prompt_lens_host, const int32_t* prompt_tokens,
+                trie_handle** out, cudaStream_t stream);
+
+/* Re-initialise the metadata from the stored prompts (same as trie_create, async). */
+int trie_reset(trie_handle* h, cudaStream_t stream);
+
+int trie_destroy(trie_handle* h);
+
+int trie_get_arrays(const trie_handle* h, trie_arrays* out);
+
+/*
+ * a-1: position-integrity RoPE + write-before-read KV append (§3.4; Alg. 3 l.7
+ * "allow attention to current node" P:175).  For request r, live beam j:
+ * pos = depth[leaf[r][j]]; q[r][j] (all Hq heads) and k_new[r][j] are rotated in place
+ * (rotate-half pairs (i, i+D/2), theta_i = rope_theta^(-2i/D), angle evaluated in fp64)
+ * and k, v are stored at slot leaf[r][j] of the layer's pools.
+ * q: [R][b_live][Hq][D] in/out; k_new, v_new: [R][b_live][Hkv][D] (k_new is rotated in
+ * place as well); k_pool, v_pool: the layer's [R][Hkv][capacity][D] pools.
+ */
+int trie_rope_kv_append(trie_handle* h, void* q, void* k_new, const void* v_new,
+                        void* k_pool, void* v_pool, float rope_theta, cudaStream_t stream);
+
+/*
+ * a-3: trie attention decode (§3.3 P:188-196 tree attention; Alg. 3 mask P:165-186).
+ * Pure function of its arguments.  For request r, live beam j, query head hq
+ * (KV head hq / (Hq/Hkv)):
+ *   o = sum_{n in A_rj} softmax_n(q . k_n / sqrt(D)) v_n,
+ *   A_rj = { n < N_r : (n < t_r or bit j of beam_mask[r][n]) and
+ *            (window == 0 or depth[r][n] >= depth[r][leaf_rj] - window + 1) }.
+ * Masked keys are excluded exactly (weight 0, reading R22).  Every unique KV row is
+ * read from HBM once per (request, KV head) and serves all b_live * (Hq/Hkv) queries.
+ * beam_mask == NULL: the mask is derived from parent[] by per-leaf walks (Alg. 3) into
+ * the scratch; otherwise parent may be NULL.
+ * q, out: [R][b_live][Hq][D]; lse (optional, may be NULL): [R][b_live][Hq] float,
+ * natural-log sum of exp of the scaled scores.  rows_hint: expected max N over requests
+ * (sizes the split-K grid; 0 = capacity).  scratch: >= trie_attn_scratch_bytes().
+ */
+size_t trie_attn_scratch_bytes(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint);
+int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const void* k_pool,
+                     const void* v_pool, const int32_t* prompt_len, const int32_t* parent,
+                     const int32_t* depth, const int32_t* leaf_ids, const int32_t* n_nodes,
+                     const uint32_t* beam_mask, int32_t window, int32_t rows_hint, void* out,
+                     float* lse, void* scratch, size_t scratch_bytes, cudaStream_t stream);
+
+/*
+ * a-4 + a-5 (+ a-2 update): one beam step (Alg. 2 l.9-11; Alg. 1 l.6 P:116).
+ * logits [R][b_live][V] fp32 (b_live = 1 on the first call).  Per request:
+ *   lp_j[v] = x_j[v] - lse_j,  lse_j = max + log sum exp(x_j - max);
+ *   the b best candidates (score_j + lp_j[v], v, j) in the total order score desc,
+ *   token asc, beam asc (readings R1, R3) are selected, in rank order;
+ *   rank r is appended at slot N + r with token v, parent leaf[j], depth[parent] + 1
+ *   (§3.4), leaves := the new slots, scores := the new scores, N += b;
+ *   beam_mask: new[n] bit r = old[n] bit j_r for every generated node (update_mask,
+ *   P:197-198), new leaf r gets bit r.
+ * Outputs (optional, may be NULL): sel_parent_beam, sel_token int32 [R][b], new_score
+ * float [R][b].
+ */
+int trie_beam_step(trie_handle* h, const float* logits, int32_t* sel_parent_beam,
+                   int32_t* sel_token, float* new_score, cudaStream_t stream);
+
+/* a-5 alone (teacher forcing): append the given selections [R][b] exactly as above. */
+int trie_append(trie_handle* h, const int32_t* sel_parent_beam, const int32_t* sel_token,
+                const float* new_score, cudaStream_t stream);
+
+/*
+ * a-6: garbage collection (§3.5 Marking / Pruning / Compaction; Alg. 2 l.5-7).
+ * keep[n] = n < t or beam_mask[n] != 0 (= n is an ancestor-or-self of a live leaf);
+ * new[n] = exclusive prefix sum of keep (stable, the paper's index_select order);
+ * token/depth/beam_mask move to new[n], parent' = new[parent], leaf' = new[leaf],
+ * N' = sum keep; in every layer the K/V rows of moved nodes are copied n -> new[n].
+ * k_pools_host / v_pools_host: host arrays of L device pointers (each layer's pool).
+ * The caller decides the schedule (every g steps; the hot path uses g = 1).
+ */
+int trie_prune_compact(trie_handle* h, void* const* k_pools_host, void* const* v_pools_host,
+                       cudaStream_t stream);
+
+/*
+ * Alg. 2 l.14 / Alg. 1 l.8: read every live hypothesis (rank order; rank 0
+ * is the best).  tokens_host [R][b][max_len] (root-to-leaf tokens, prompt included,
+ * padded with -1), len_host [R][b], score_host [R][b].  Synchronises the stream.
+ */
+int trie_read_hyps(trie_handle* h, int32_t max_len, int32_t* tokens_host, int32_t* len_host,
+                   float* score_host, void* scratch, size_t scratch_bytes, cudaStream_t stream);
+
+/* Read (and keep) the latched device status bits.  Synchronises the stream. */
+int trie_status(trie_handle* h, uint32_t* bits_host, cudaStream_t stream);
+
+const char* trie_last_error(void);
+
+/* library version (major << 16 | minor) */
+int trie_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRIEDECODE_H */

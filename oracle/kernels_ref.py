@@ -14,12 +14,15 @@ from .trie import Trie, build_mask, garbage_collect, update_mask, window_allow
 
 
 # ---- integer path ----------------------------------------------------------------------
-def build_tries(prompts, prompt_lens, sel_seq, b: int, g=1, final_gc=True):
+def build_tries(prompts, prompt_lens, sel_seq, b: int, g=1, final_gc=True, t_sched=None):
     """Teacher-forced trie evolution for R requests: for each step k apply the given
     (parent_beam, token) selection with update_trie (Alg. 2 l.10), then GC iff
     (t + k) mod g == 0 (reading R7/R8: Alg. 2's top-of-iteration check, placed after the
     append of step k; `final_gc` also applies it after the last step).
-    sel_seq[k] = (parent[R][b_k], token[R][b_k]).  Returns a list of Trie."""
+    sel_seq[k] = (parent[R][b_k], token[R][b_k]).  t_sched (default: each request's own t)
+    replaces t in the schedule test, for batched drivers that share one schedule across
+    ragged prompts (GC timing never changes outputs, only when memory is reclaimed).
+    Returns a list of Trie."""
     tries = []
     for r in range(len(prompt_lens)):
         T = Trie(prompts[r][: prompt_lens[r]])
@@ -28,7 +31,8 @@ def build_tries(prompts, prompt_lens, sel_seq, b: int, g=1, final_gc=True):
             sel = [(0.0, int(tok[r][i]), int(par[r][i])) for i in range(len(par[r]))]
             T.update_trie(sel)
             last = k == steps
-            if g is not None and (T.t + k) % g == 0 and (final_gc or not last):
+            tt = T.t if t_sched is None else t_sched
+            if g is not None and (tt + k) % g == 0 and (final_gc or not last):
                 garbage_collect(T)
         tries.append(T)
     return tries

@@ -1,0 +1,367 @@
+// C ABI glue of libtriedecode: argument validation, workspace carving, dispatch.
+// Every step of the hot path runs in the kernels of this library; there is no CPU path.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+
+#include "attn_common.cuh"
+#include "common.cuh"
+#include "handle.h"
+
+static thread_local char g_err[512] = "";
+
+int trie_set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int trie_check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return trie_set_error(TRIE_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return TRIE_OK;
+}
+
+static int validate(const trie_cfg* c) {
+  if (!c) return trie_set_error(TRIE_EINVAL, "null cfg");
+  if (c->n_requests < 1) return trie_set_error(TRIE_EINVAL, "n_requests < 1");
+  if (c->beam_width < 1 || c->beam_width > TRIE_MAX_BEAMS)
+    return trie_set_error(TRIE_EINVAL, "beam_width %d not in [1, 32]", c->beam_width);
+  if (c->vocab < c->beam_width) return trie_set_error(TRIE_EINVAL, "beam_width > vocab");
+  if (c->max_prompt_len < 1) return trie_set_error(TRIE_EINVAL, "max_prompt_len < 1");
+  if (c->capacity < c->max_prompt_len + c->beam_width)
+    return trie_set_error(TRIE_EINVAL, "capacity < max_prompt_len + beam_width");
+  if (c->n_layers < 0 || c->n_layers > TRIE_MAX_LAYERS)
+    return trie_set_error(TRIE_EINVAL, "n_layers not in [0, %d]", TRIE_MAX_LAYERS);
+  if (c->n_q_heads < 1 || c->n_kv_heads < 1 || c->n_q_heads % c->n_kv_heads)
+    return trie_set_error(TRIE_EINVAL, "n_q_heads %% n_kv_heads != 0 (GQA, S:104)");
+  if (c->head_dim < 16 || c->head_dim > 256 || c->head_dim % 16)
+    return trie_set_error(TRIE_EINVAL, "head_dim must be a multiple of 16 in [16, 256]");
+  if (c->window < 0) return trie_set_error(TRIE_EINVAL, "window < 0");
+  if (c->kv_dtype != TRIE_F32 && c->kv_dtype != TRIE_BF16)
+    return trie_set_error(TRIE_EINVAL, "kv_dtype");
+  return TRIE_OK;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
+  const size_t R = c->n_requests, cap = c->capacity, b = c->beam_width;
+  const size_t chunks = (c->vocab + 4095) / 4096;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  char* token = take(R * cap * 4);
+  char* parent = take(R * cap * 4);
+  char* depth = take(R * cap * 4);
+  char* mask = take(R * cap * 4);
+  char* leaf = take(R * TRIE_MAX_BEAMS * 4);
+  char* score = take(R * TRIE_MAX_BEAMS * 4);
+  char* nn = take(R * 4);
+  char* nkv = take(R * 4);
+  char* tlen = take(R * 4);
+  char* status = take(4);
+  char* prompts = take(R * c->max_prompt_len * 4);
+  char* newidx = take(R * cap * 4);
+  char* moves = take(R * cap * 4);
+  char* nmoves = take(R * 4);
+  char* cmax = take(R * b * chunks * 4);
+  char* csum = take(R * b * chunks * 4);
+  char* ctop = take(R * b * chunks * b * 8);
+  char* sp = take(R * b * 4);
+  char* st = take(R * b * 4);
+  char* ss = take(R * b * 4);
+  if (h) {
+    h->token = (int32_t*)token;
+    h->parent = (int32_t*)parent;
+    h->depth = (int32_t*)depth;
+    h->mask = (uint32_t*)mask;
+    h->leaf = (int32_t*)leaf;
+    h->score = (float*)score;
+    h->n_nodes = (int32_t*)nn;
+    h->n_kv = (int32_t*)nkv;
+    h->tlen = (int32_t*)tlen;
+    h->status = (uint32_t*)status;
+    h->prompts = (int32_t*)prompts;
+    h->newidx = (int32_t*)newidx;
+    h->moves = (int32_t*)moves;
+    h->n_moves = (int32_t*)nmoves;
+    h->chunk_max = (float*)cmax;
+    h->chunk_sum = (float*)csum;
+    h->chunk_top = (uint64_t*)ctop;
+    h->sel_parent = (int32_t*)sp;
+    h->sel_token = (int32_t*)st;
+    h->sel_score = (float*)ss;
+    h->chunks = (int32_t)chunks;
+  }
+  return off;
+}
+
+extern "C" {
+
+int trie_version(void) { return (1 << 16) | 0; }
+
+const char* trie_last_error(void) { return g_err; }
+
+int trie_workspace_bytes(const trie_cfg* cfg, size_t* bytes) {
+  int rc = validate(cfg);
+  if (rc) return rc;
+  if (!bytes) return trie_set_error(TRIE_EINVAL, "null bytes");
+  *bytes = trie_layout(cfg, nullptr, nullptr);
+  return TRIE_OK;
+}
+
+int trie_create(const trie_cfg* cfg, void* workspace, size_t workspace_bytes,
+                const int32_t* prompt_lens_host, const int32_t* prompt_tokens,
+                trie_handle** out, cudaStream_t stream) {
+  int rc = validate(cfg);
+  if (rc) return rc;
+  if (!workspace || !prompt_lens_host || !prompt_tokens || !out)
+    return trie_set_error(TRIE_EINVAL, "null argument");
+  const size_t need = trie_layout(cfg, nullptr, nullptr);
+  if (workspace_bytes < need)
+    return trie_set_error(TRIE_ECAPACITY, "workspace %zu < %zu bytes", workspace_bytes, need);
+  if ((uintptr_t)workspace % 256)
+    return trie_set_error(TRIE_EINVAL, "workspace must be 256-byte aligned");
+  for (int r = 0; r < cfg->n_requests; ++r) {
+    const int t = prompt_lens_host[r];
+    if (t < 1) return trie_set_error(TRIE_EINVAL, "empty prompt for request %d (S:260)", r);
+    if (t > cfg->max_prompt_len)
+      return trie_set_error(TRIE_EINVAL, "prompt %d longer than max_prompt_len", r);
+  }
+  trie_handle* h = new (std::nothrow) trie_handle();
+  if (!h) return trie_set_error(TRIE_EINVAL, "out of host memory");
+  h->cfg = *cfg;
+  h->ws = (char*)workspace;
+  h->ws_bytes = workspace_bytes;
+  trie_layout(cfg, h, (char*)workspace);
+  h->host_tlen.assign(prompt_lens_host, prompt_lens_host + cfg->n_requests);
+  cudaError_t e = cudaMemcpyAsync(h->tlen, prompt_lens_host, cfg->n_requests * 4,
+                                  cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h->prompts, prompt_tokens,
+                        (size_t)cfg->n_requests * cfg->max_prompt_len * 4,
+                        cudaMemcpyDeviceToDevice, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->status, 0, 4, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // prompt_lens_host may be freed
+  if (e != cudaSuccess) {
+    delete h;
+    return trie_set_error(TRIE_ECUDA, "trie_create: %s", cudaGetErrorString(e));
+  }
+  rc = trie::launch_init(h, stream);
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return TRIE_OK;
+}
+
+int trie_reset(trie_handle* h, cudaStream_t stream) {
+  if (!h) return trie_set_error(TRIE_EINVAL, "null handle");
+  h->b_live = 1;
+  h->steps = 0;
+  return trie::launch_init(h, stream);
+}
+
+int trie_destroy(trie_handle* h) {
+  delete h;
+  return TRIE_OK;
+}
+
+int trie_get_arrays(const trie_handle* h, trie_arrays* o) {
+  if (!h || !o) return trie_set_error(TRIE_EINVAL, "null argument");
+  o->token = h->token;
+  o->parent = h->parent;
+  o->depth = h->depth;
+  o->beam_mask = h->mask;
+  o->leaf = h->leaf;
+  o->score = h->score;
+  o->n_nodes = h->n_nodes;
+  o->prompt_len = h->tlen;
+  o->status = h->status;
+  o->b_live = h->b_live;
+  o->steps = h->steps;
+  return TRIE_OK;
+}
+
+int trie_rope_kv_append(trie_handle* h, void* q, void* k_new, const void* v_new, void* k_pool,
+                        void* v_pool, float rope_theta, cudaStream_t stream) {
+  if (!h || !q || !k_new || !v_new || !k_pool || !v_pool)
+    return trie_set_error(TRIE_EINVAL, "null argument");
+  if (!(rope_theta > 1.f)) return trie_set_error(TRIE_EINVAL, "rope_theta must be > 1");
+  return trie::launch_rope_append(h, q, k_new, v_new, k_pool, v_pool, rope_theta, stream);
+}
+
+// ---- attention ------------------------------------------------------------------------
+static int attn_splits(const trie_cfg* c, int rows_hint) {
+  int rows = rows_hint > 0 ? rows_hint : c->capacity;
+  const int units = c->n_requests * c->n_kv_heads;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int target = sms * 2;  // two resident CTAs per SM
+  int splits = (target + units - 1) / units;
+  const int max_by_rows = rows / 128 > 0 ? rows / 128 : 1;  // >= 128 rows per split
+  if (splits > max_by_rows) splits = max_by_rows;
+  if (splits > 64) splits = 64;
+  return splits < 1 ? 1 : splits;
+}
+
+static size_t part_bytes(const trie_cfg* c, int b_live, int splits) {
+  if (splits <= 1) return 0;
+  const size_t Qg = (size_t)b_live * (c->n_q_heads / c->n_kv_heads);
+  return (size_t)c->n_requests * c->n_kv_heads * splits * Qg * (c->head_dim + 2) * 4;
+}
+
+size_t trie_attn_scratch_bytes(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint) {
+  if (validate(cfg)) return 0;
+  const int splits = attn_splits(cfg, rows_hint);
+  // split partials + a derived beam_mask when the caller passes none
+  return align_up(part_bytes(cfg, b_live, splits)) +
+         align_up((size_t)cfg->n_requests * cfg->capacity * 4) + 256;
+}
+
+int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const void* k_pool,
+                     const void* v_pool, const int32_t* prompt_len, const int32_t* parent,
+                     const int32_t* depth, const int32_t* leaf_ids, const int32_t* n_nodes,
+                     const uint32_t* beam_mask, int32_t window, int32_t rows_hint, void* out,
+                     float* lse, void* scratch, size_t scratch_bytes, cudaStream_t stream) {
+  int rc = validate(cfg);
+  if (rc) return rc;
+  if (b_live < 1 || b_live > cfg->beam_width) return trie_set_error(TRIE_EINVAL, "b_live");
+  if (!q || !k_pool || !v_pool || !prompt_len || !depth || !leaf_ids || !n_nodes || !out)
+    return trie_set_error(TRIE_EINVAL, "null argument");
+  if (window < 0) return trie_set_error(TRIE_EINVAL, "window < 0");
+  const int splits = attn_splits(cfg, rows_hint);
+  const size_t pb = align_up(part_bytes(cfg, b_live, splits));
+  const size_t mb = align_up((size_t)cfg->n_requests * cfg->capacity * 4);
+  const size_t need = pb + (beam_mask ? 0 : mb);
+  if (need > 0 && (!scratch || scratch_bytes < need))
+    return trie_set_error(TRIE_ECAPACITY, "attention scratch %zu < %zu", scratch_bytes, need);
+  if (!beam_mask) {
+    if (!parent) return trie_set_error(TRIE_EINVAL, "beam_mask == NULL needs parent[]");
+    uint32_t* derived = (uint32_t*)((char*)scratch + pb);
+    rc = trie::launch_mask_walk(cfg, b_live, prompt_len, parent, leaf_ids, n_nodes, derived,
+                                nullptr, stream);
+    if (rc) return rc;
+    beam_mask = derived;
+  }
+  trie::AttnParams p;
+  p.q = q;
+  p.k = k_pool;
+  p.v = v_pool;
+  p.out = out;
+  p.lse = lse;
+  p.tlen = prompt_len;
+  p.depth = depth;
+  p.leaf = leaf_ids;
+  p.nn = n_nodes;
+  p.mask = beam_mask;
+  p.part = (float*)scratch;
+  p.status = nullptr;
+  p.R = cfg->n_requests;
+  p.b_live = b_live;
+  p.Hq = cfg->n_q_heads;
+  p.Hkv = cfg->n_kv_heads;
+  p.D = cfg->head_dim;
+  p.cap = cfg->capacity;
+  p.window = window;
+  p.splits = splits;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)cfg->head_dim);
+  p.bf16 = cfg->kv_dtype == TRIE_BF16;
+  return trie::launch_attn_v1(p, stream);
+}
+
+// ---- beam step / append / prune --------------------------------------------------------
+int trie_beam_step(trie_handle* h, const float* logits, int32_t* sel_parent_beam,
+                   int32_t* sel_token, float* new_score, cudaStream_t stream) {
+  if (!h || !logits) return trie_set_error(TRIE_EINVAL, "null argument");
+  int rc = trie::launch_beam_step(h, logits, stream);
+  if (rc) return rc;
+  const size_t n = (size_t)h->cfg.n_requests * h->cfg.beam_width * 4;
+  cudaError_t e = cudaSuccess;
+  if (sel_parent_beam)
+    e = cudaMemcpyAsync(sel_parent_beam, h->sel_parent, n, cudaMemcpyDeviceToDevice, stream);
+  if (e == cudaSuccess && sel_token)
+    e = cudaMemcpyAsync(sel_token, h->sel_token, n, cudaMemcpyDeviceToDevice, stream);
+  if (e == cudaSuccess && new_score)
+    e = cudaMemcpyAsync(new_score, h->sel_score, n, cudaMemcpyDeviceToDevice, stream);
+  if (e != cudaSuccess) return trie_set_error(TRIE_ECUDA, "beam_step copy: %s", cudaGetErrorString(e));
+  h->b_live = h->cfg.beam_width;
+  h->steps += 1;
+  return TRIE_OK;
+}
+
+int trie_append(trie_handle* h, const int32_t* sel_parent_beam, const int32_t* sel_token,
+                const float* new_score, cudaStream_t stream) {
+  if (!h || !sel_parent_beam || !sel_token) return trie_set_error(TRIE_EINVAL, "null argument");
+  int rc = trie::launch_append(h, sel_parent_beam, sel_token, new_score, stream);
+  if (rc) return rc;
+  h->b_live = h->cfg.beam_width;
+  h->steps += 1;
+  return TRIE_OK;
+}
+
+int trie_prune_compact(trie_handle* h, void* const* k_pools_host, void* const* v_pools_host,
+                       cudaStream_t stream) {
+  if (!h) return trie_set_error(TRIE_EINVAL, "null handle");
+  if (h->cfg.n_layers > 0 && (!k_pools_host || !v_pools_host))
+    return trie_set_error(TRIE_EINVAL, "null pool pointer arrays");
+  if (h->steps == 0) return TRIE_OK;  // nothing appended yet: the prompt chain is all live
+  return trie::launch_prune(h, k_pools_host, v_pools_host, stream);
+}
+
+int trie_read_hyps(trie_handle* h, int32_t max_len, int32_t* tokens_host, int32_t* len_host,
+                   float* score_host, void* scratch, size_t scratch_bytes, cudaStream_t stream) {
+  if (!h || max_len < 1) return trie_set_error(TRIE_EINVAL, "bad argument");
+  const int R = h->cfg.n_requests, b = h->b_live;
+  const size_t need = (size_t)R * b * (max_len + 1) * 4;
+  if (!scratch || scratch_bytes < need)
+    return trie_set_error(TRIE_ECAPACITY, "read_hyps scratch %zu < %zu", scratch_bytes, need);
+  int rc = trie::launch_read_hyps(h, max_len, (int32_t*)scratch, stream);
+  if (rc) return rc;
+  int32_t* tmp = new (std::nothrow) int32_t[(size_t)R * b * (max_len + 1)];
+  float* sc = new (std::nothrow) float[(size_t)R * TRIE_MAX_BEAMS];
+  if (!tmp || !sc) {
+    delete[] tmp;
+    delete[] sc;
+    return trie_set_error(TRIE_EINVAL, "out of host memory");
+  }
+  cudaError_t e = cudaMemcpyAsync(tmp, scratch, need, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(sc, h->score, (size_t)R * TRIE_MAX_BEAMS * 4, cudaMemcpyDeviceToHost,
+                        stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e == cudaSuccess) {
+    for (int r = 0; r < R; ++r)
+      for (int j = 0; j < b; ++j) {
+        const int32_t* src = tmp + ((size_t)r * b + j) * (max_len + 1);
+        if (len_host) len_host[r * b + j] = src[0];
+        if (tokens_host) memcpy(tokens_host + ((size_t)r * b + j) * max_len, src + 1, max_len * 4);
+        if (score_host) score_host[r * b + j] = sc[r * TRIE_MAX_BEAMS + j];
+      }
+  }
+  delete[] tmp;
+  delete[] sc;
+  if (e != cudaSuccess) return trie_set_error(TRIE_ECUDA, "read_hyps: %s", cudaGetErrorString(e));
+  return TRIE_OK;
+}
+
+int trie_status(trie_handle* h, uint32_t* bits_host, cudaStream_t stream) {
+  if (!h || !bits_host) return trie_set_error(TRIE_EINVAL, "null argument");
+  cudaError_t e = cudaMemcpyAsync(bits_host, h->status, 4, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return trie_set_error(TRIE_ECUDA, "status: %s", cudaGetErrorString(e));
+  return TRIE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,29 @@
+// Parameters shared by the trie attention kernels (attn_decode.cu, attn_decode_tc.cu).
+#pragma once
+#include <stdint.h>
+
+namespace trie {
+
+struct AttnParams {
+  const void* q;       // [R][b_live][Hq][D]
+  const void* k;       // [R][Hkv][cap][D]
+  const void* v;       // [R][Hkv][cap][D]
+  void* out;           // [R][b_live][Hq][D]
+  float* lse;          // [R][b_live][Hq] or null
+  const int32_t* tlen; // [R]
+  const int32_t* depth;   // [R][cap]
+  const int32_t* leaf;    // [R][32]
+  const int32_t* nn;      // [R]
+  const uint32_t* mask;   // [R][cap]
+  float* part;            // split partials
+  uint32_t* status;
+  int R, b_live, Hq, Hkv, D, cap, window, splits;
+  float scale_log2;       // log2(e) / sqrt(D)
+  int bf16;
+};
+
+int launch_attn_v1(const AttnParams& p, cudaStream_t s);
+int launch_attn_tc(const AttnParams& p, cudaStream_t s);  // returns 1 if shape unsupported
+size_t attn_tc_part_bytes(const AttnParams& p);
+
+}  // namespace trie

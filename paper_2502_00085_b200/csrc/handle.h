@@ -1,0 +1,61 @@
+// Internal: the host-side handle and workspace carving of libtriedecode.
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/triedecode.h"
+
+struct trie_handle {
+  trie_cfg cfg;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  // trie metadata, SoA [R][cap]
+  int32_t* token = nullptr;
+  int32_t* parent = nullptr;
+  int32_t* depth = nullptr;
+  uint32_t* mask = nullptr;
+  int32_t* leaf = nullptr;    // [R][32]
+  float* score = nullptr;     // [R][32]
+  int32_t* n_nodes = nullptr; // [R]
+  int32_t* n_kv = nullptr;    // [R] slots [0, n_kv) hold K/V (pending leaves do not)
+  int32_t* tlen = nullptr;    // [R]
+  uint32_t* status = nullptr; // [1]
+  int32_t* prompts = nullptr; // [R][t_max]
+  // prune scratch
+  int32_t* newidx = nullptr;  // [R][cap]
+  int32_t* moves = nullptr;   // [R][cap]
+  int32_t* n_moves = nullptr; // [R]
+  // beam-step scratch
+  float* chunk_max = nullptr;     // [R][b][chunks]
+  float* chunk_sum = nullptr;     // [R][b][chunks]
+  uint64_t* chunk_top = nullptr;  // [R][b][chunks][b]  key = ord(x) << 32 | ~v
+  int32_t* sel_parent = nullptr;  // [R][b]
+  int32_t* sel_token = nullptr;   // [R][b]
+  float* sel_score = nullptr;     // [R][b]
+  int32_t chunks = 1;
+  int32_t chunk_len = 4096;
+  // host-tracked state
+  int32_t b_live = 1;
+  int32_t steps = 0;
+  std::vector<int32_t> host_tlen;
+};
+
+// carve the workspace; with h == nullptr only computes the size
+size_t trie_layout(const trie_cfg* cfg, trie_handle* h, char* base);
+
+// launchers (defined in the .cu files)
+namespace trie {
+int launch_init(trie_handle* h, cudaStream_t s);
+int launch_append(trie_handle* h, const int32_t* par, const int32_t* tok, const float* sc,
+                  cudaStream_t s);
+int launch_beam_step(trie_handle* h, const float* logits, cudaStream_t s);
+int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t s);
+int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, void* kpool,
+                       void* vpool, float theta, cudaStream_t s);
+int launch_read_hyps(trie_handle* h, int32_t max_len, int32_t* out_dev, cudaStream_t s);
+int launch_mask_walk(const trie_cfg* cfg, int32_t b_live, const int32_t* tlen,
+                     const int32_t* parent, const int32_t* leaf, const int32_t* nn,
+                     uint32_t* mask_out, uint32_t* status, cudaStream_t s);
+}  // namespace trie

@@ -1,0 +1,287 @@
+// Trie metadata kernels: initialize_trie (Alg. 2 l.1), garbage collection (§3.5:
+// marking / pruning / compaction), hypothesis read-out (Alg. 2 l.14) and the
+// Alg. 3 parent walk that derives beam bitsets when the caller passes no beam_mask.
+#include <stdio.h>
+
+#include "common.cuh"
+#include "handle.h"
+
+namespace trie {
+
+// exclusive block scan of one int per thread; returns prefix, writes block total
+template <int BS>
+__device__ __forceinline__ int block_excl_scan(int v, int* total, int* sm_warp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int s = lane < BS / 32 ? sm_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < BS / 32) sm_warp[lane] = s;  // inclusive warp-total prefix
+  }
+  __syncthreads();
+  int before = (w > 0 ? sm_warp[w - 1] : 0) + x - v;
+  *total = sm_warp[BS / 32 - 1];
+  __syncthreads();
+  return before;
+}
+
+// ---- Alg. 2 l.1 initialize_trie(prompt) --------------------------------------------------
+__global__ void k_init(int32_t* token, int32_t* parent, int32_t* depth, uint32_t* mask,
+                       int32_t* leaf, float* score, int32_t* nn, int32_t* nkv,
+                       const int32_t* tlen, const int32_t* prompts, int t_max, int cap) {
+  const int r = blockIdx.x;
+  const int t = tlen[r];
+  const size_t base = (size_t)r * cap;
+  for (int i = threadIdx.x; i < t; i += blockDim.x) {
+    token[base + i] = prompts[(size_t)r * t_max + i];
+    parent[base + i] = i - 1;
+    depth[base + i] = i;  // §3.4: position of the conventional sequence
+    mask[base + i] = 0u;  // prompt columns are implicitly allowed for every beam
+  }
+  if (threadIdx.x == 0) {
+    leaf[r * TRIE_MAX_BEAMS] = t - 1;
+    score[r * TRIE_MAX_BEAMS] = 0.f;
+    nn[r] = t;
+    nkv[r] = t;  // the prompt's K/V come from the caller's prefill
+  }
+}
+
+int launch_init(trie_handle* h, cudaStream_t s) {
+  const trie_cfg& c = h->cfg;
+  k_init<<<c.n_requests, 256, 0, s>>>(h->token, h->parent, h->depth, h->mask, h->leaf, h->score,
+                                      h->n_nodes, h->n_kv, h->tlen, h->prompts,
+                                      c.max_prompt_len, c.capacity);
+  return trie_check_launch("k_init");
+}
+
+// ---- §3.5 GC: keep-scan + stable metadata compaction + move list ----------------------
+// One CTA per request.  keep[n] = n < t or beam_mask[n] != 0 (n is an ancestor-or-self
+// of a live leaf: the bits are exactly Alg. 3's rows, see beam_step.cu).  new[n] =
+// exclusive prefix sum of keep.  In-place compaction moves every kept row to a lower or
+// equal slot; processing rows in ascending batches, each batch read-all -> barrier ->
+// write-all, is race free (a write target new[n] <= n never belongs to a later batch).
+constexpr int PRUNE_BS = 512;
+__global__ void __launch_bounds__(PRUNE_BS) k_prune_scan(
+    int32_t* token, int32_t* parent, int32_t* depth, uint32_t* mask, int32_t* leaf,
+    int32_t* nn, const int32_t* nkv, const int32_t* tlen, int32_t* newidx, int32_t* moves,
+    int32_t* n_moves, int b_live, int cap, uint32_t* status) {
+  __shared__ int sm_warp[32];
+  const int r = blockIdx.x;
+  const int N = nn[r], t = tlen[r], n_kv = nkv[r];
+  const size_t base = (size_t)r * cap;
+  int32_t* nidx = newidx + base;
+  // pass 1: scan
+  int carry = t;
+  for (int b0 = t; b0 < N; b0 += PRUNE_BS) {
+    const int n = b0 + threadIdx.x;
+    const int keep = (n < N && mask[base + n] != 0u) ? 1 : 0;
+    int tot;
+    const int pre = block_excl_scan<PRUNE_BS>(keep, &tot, sm_warp);
+    if (n < N) nidx[n] = keep ? carry + pre : -1;
+    carry += tot;
+  }
+  const int N_new = carry;
+  __syncthreads();
+  // pass 2: compaction in ascending batches + ordered move list
+  int mcarry = 0;
+  for (int b0 = t; b0 < N; b0 += PRUNE_BS) {
+    const int n = b0 + threadIdx.x;
+    int dst = -1, tok = 0, par = 0, dep = 0;
+    uint32_t msk = 0;
+    if (n < N) {
+      dst = nidx[n];
+      if (dst >= 0) {
+        tok = token[base + n];
+        const int p = parent[base + n];
+        dep = depth[base + n];
+        msk = mask[base + n];
+        if (p < 0 || p >= n) {
+          latch(status, TRIE_ST_PARENT);
+          par = -1;
+        } else {
+          par = p < t ? p : nidx[p];
+          if (par < 0) latch(status, TRIE_ST_PARENT);  // kept node with a dropped parent
+        }
+      }
+    }
+    const int mv = (dst >= 0 && dst != n && n < n_kv) ? 1 : 0;
+    int mtot;
+    const int mpre = block_excl_scan<PRUNE_BS>(mv, &mtot, sm_warp);  // contains barriers
+    if (dst >= 0) {
+      token[base + dst] = tok;
+      parent[base + dst] = par;
+      depth[base + dst] = dep;
+      mask[base + dst] = msk;
+    }
+    if (mv) moves[base + mcarry + mpre] = n;
+    mcarry += mtot;
+    __syncthreads();
+  }
+  if (threadIdx.x < b_live) {
+    const int l = leaf[r * TRIE_MAX_BEAMS + threadIdx.x];
+    const int nl = (l >= 0 && l < N) ? (l < t ? l : nidx[l]) : -1;
+    if (nl < 0) latch(status, TRIE_ST_LEAF);
+    leaf[r * TRIE_MAX_BEAMS + threadIdx.x] = nl < 0 ? 0 : nl;
+  }
+  if (threadIdx.x == 0) {
+    nn[r] = N_new;
+    n_moves[r] = mcarry;
+  }
+}
+
+// ---- §3.5 Compaction of the KV cache (the paper's index_select) -----------------
+// One CTA per (request, layer); all KV heads of a moved slot are copied with 16-byte
+// vectors.  Moves are applied in ascending batches (read-all, barrier, write-all) for
+// the same in-place safety argument as above.
+struct PoolPtrs {
+  void* k[TRIE_MAX_LAYERS];
+  void* v[TRIE_MAX_LAYERS];
+};
+
+constexpr int COMPACT_BS = 256;
+constexpr int COMPACT_VEC = 4;  // 16-byte vectors in flight per thread per batch
+__global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant__ PoolPtrs pp,
+                                                           const int32_t* moves,
+                                                           const int32_t* n_moves,
+                                                           const int32_t* newidx, int Hkv,
+                                                           int row_bytes, int cap) {
+  const int r = blockIdx.x, layer = blockIdx.y;
+  const int nm = n_moves[r];
+  if (nm == 0) return;
+  const size_t base = (size_t)r * cap;
+  const int vec_per_row = row_bytes / 16;                // one (head, slot) row
+  const int vec_per_slot = 2 * Hkv * vec_per_row;       // K and V, all heads
+  char* kb = (char*)pp.k[layer] + (size_t)r * Hkv * cap * row_bytes;
+  char* vb = (char*)pp.v[layer] + (size_t)r * Hkv * cap * row_bytes;
+  const int per_batch = COMPACT_BS * COMPACT_VEC;
+  const long total = (long)nm * vec_per_slot;
+  for (long b0 = 0; b0 < total; b0 += per_batch) {
+    // batches must not split a slot's reads from an earlier slot's writes in a racy way:
+    // all reads of the batch happen before all its writes (barrier below); batches are
+    // ascending in move order, so later reads never hit earlier-written targets' sources.
+    int4 val[COMPACT_VEC];
+    char* dstp[COMPACT_VEC];
+#pragma unroll
+    for (int u = 0; u < COMPACT_VEC; ++u) {
+      const long e = b0 + (long)u * COMPACT_BS + threadIdx.x;
+      dstp[u] = nullptr;
+      if (e < total) {
+        const int mi = (int)(e / vec_per_slot);
+        int rem = (int)(e % vec_per_slot);
+        const int kv = rem / (Hkv * vec_per_row);
+        rem -= kv * Hkv * vec_per_row;
+        const int hh = rem / vec_per_row, c = rem % vec_per_row;
+        const int src = moves[base + mi];
+        const int dst = newidx[base + src];
+        char* pool = kv ? vb : kb;
+        const size_t hoff = (size_t)hh * cap * row_bytes + (size_t)c * 16;
+        val[u] = *(const int4*)(pool + hoff + (size_t)src * row_bytes);
+        dstp[u] = pool + hoff + (size_t)dst * row_bytes;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < COMPACT_VEC; ++u)
+      if (dstp[u]) *(int4*)dstp[u] = val[u];
+    __syncthreads();
+  }
+}
+
+int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t s) {
+  const trie_cfg& c = h->cfg;
+  k_prune_scan<<<c.n_requests, PRUNE_BS, 0, s>>>(h->token, h->parent, h->depth, h->mask,
+                                                 h->leaf, h->n_nodes, h->n_kv, h->tlen,
+                                                 h->newidx, h->moves, h->n_moves, h->b_live,
+                                                 c.capacity, h->status);
+  int rc = trie_check_launch("k_prune_scan");
+  if (rc) return rc;
+  if (c.n_layers == 0 || kp == nullptr) return TRIE_OK;
+  PoolPtrs pp;
+  for (int l = 0; l < c.n_layers; ++l) {
+    pp.k[l] = kp[l];
+    pp.v[l] = vp[l];
+  }
+  const int esz = c.kv_dtype == TRIE_BF16 ? 2 : 4;
+  dim3 grid(c.n_requests, c.n_layers);
+  k_kv_compact<<<grid, COMPACT_BS, 0, s>>>(pp, h->moves, h->n_moves, h->newidx, c.n_kv_heads,
+                                           c.head_dim * esz, c.capacity);
+  return trie_check_launch("k_kv_compact");
+}
+
+// ---- Alg. 2 l.14: hypotheses = root-to-leaf token paths ---------------------------------
+__global__ void k_read_hyps(const int32_t* token, const int32_t* parent, const int32_t* depth,
+                            const int32_t* leaf, int b_live, int cap, int max_len,
+                            int32_t* out) {
+  const int r = blockIdx.x, j = threadIdx.x;
+  if (j >= b_live) return;
+  int32_t* o = out + ((size_t)r * b_live + j) * (max_len + 1);
+  const size_t base = (size_t)r * cap;
+  int n = leaf[r * TRIE_MAX_BEAMS + j];
+  const int len = depth[base + n] + 1;
+  o[0] = len;
+  for (int i = 0; i < max_len; ++i) o[1 + i] = -1;
+  int guard = 0;
+  while (n >= 0 && guard++ < cap) {
+    const int d = depth[base + n];
+    if (d < max_len) o[1 + d] = token[base + n];
+    n = parent[base + n];
+  }
+}
+
+int launch_read_hyps(trie_handle* h, int32_t max_len, int32_t* out_dev, cudaStream_t s) {
+  k_read_hyps<<<h->cfg.n_requests, 32, 0, s>>>(h->token, h->parent, h->depth, h->leaf,
+                                                h->b_live, h->cfg.capacity, max_len, out_dev);
+  return trie_check_launch("k_read_hyps");
+}
+
+// ---- Alg. 3 as per-leaf walks (used when trie_attn_decode gets beam_mask == NULL) -------
+// Reading R19: the b simultaneous walkers of Alg. 3 give the same set as independent
+// per-leaf walks.  Bit j of word n is set iff generated node n lies on leaf j's path.
+__global__ void k_mask_walk(const int32_t* tlen, const int32_t* parent, const int32_t* leaf,
+                            const int32_t* nn, int b_live, int cap, uint32_t* mask_out,
+                            uint32_t* status) {
+  const int r = blockIdx.x;
+  const int t = tlen[r], N = nn[r];
+  const size_t base = (size_t)r * cap;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) mask_out[base + n] = 0u;
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < b_live) {
+    int n = leaf[r * TRIE_MAX_BEAMS + j];
+    if (n < 0 || n >= N) {
+      latch(status, TRIE_ST_LEAF);
+      return;
+    }
+    int guard = 0;
+    while (n >= t) {
+      atomicOr(&mask_out[base + n], 1u << j);
+      const int p = parent[base + n];
+      if (p >= n || p < 0 || ++guard > N) {
+        latch(status, TRIE_ST_PARENT);
+        break;
+      }
+      n = p;
+    }
+  }
+}
+
+int launch_mask_walk(const trie_cfg* c, int32_t b_live, const int32_t* tlen,
+                     const int32_t* parent, const int32_t* leaf, const int32_t* nn,
+                     uint32_t* mask_out, uint32_t* status, cudaStream_t s) {
+  k_mask_walk<<<c->n_requests, 256, 0, s>>>(tlen, parent, leaf, nn, b_live, c->capacity,
+                                            mask_out, status);
+  return trie_check_launch("k_mask_walk");
+}
+
+}  // namespace trie

@@ -1,0 +1,113 @@
+"""TrieState: owns the workspace of one trie handle and exposes the C ABI calls as methods.
+
+PyTorch only allocates device memory and provides the stream; every operation on the
+trie, the KV pools and the logits runs in libtriedecode's kernels (argument marshalling
+only here).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib as L
+
+
+class TrieState:
+    def __init__(self, R, b, t_max, capacity, n_layers, Hq, Hkv, D, V, prompt_tokens, prompt_lens,
+                 window=0, gc_interval=1, dtype=torch.bfloat16, device="cuda", stream=None):
+        if not torch.cuda.is_available():
+            raise L.TrieError("no CUDA device: libtriedecode has no CPU path")
+        self.kv_dtype = L.TRIE_BF16 if dtype == torch.bfloat16 else L.TRIE_F32
+        self.dtype = dtype
+        self.cfg = L.make_cfg(R, b, t_max, capacity, n_layers, Hq, Hkv, D, V, window, gc_interval,
+                              self.kv_dtype)
+        self.R, self.b, self.t_max, self.cap = R, b, t_max, capacity
+        self.L, self.Hq, self.Hkv, self.D, self.V, self.window = n_layers, Hq, Hkv, D, V, window
+        self.device = device
+        nbytes = L.trie_workspace_bytes(self.cfg)
+        self.ws = torch.zeros(nbytes + 256, dtype=torch.uint8, device=device)
+        off = (-self.ws.data_ptr()) % 256
+        self.ws_al = self.ws[off: off + nbytes]
+        toks = torch.as_tensor(prompt_tokens, dtype=torch.int32).reshape(R, t_max).to(device)
+        self.h = L.trie_create(self.cfg, self.ws_al, list(prompt_lens), toks, stream)
+        self._toks = toks
+        self._views()
+        self.attn_scratch = None
+        self.hyp_scratch = None
+
+    def _views(self):
+        a = L.trie_get_arrays(self.h)
+        base = self.ws_al.data_ptr()
+
+        def view(ptr, n, dt, shape):
+            o = ptr - base
+            return self.ws_al[o: o + n * 4].view(dt).view(*shape)
+        R, cap = self.R, self.cap
+        self.token = view(a.token, R * cap, torch.int32, (R, cap))
+        self.parent = view(a.parent, R * cap, torch.int32, (R, cap))
+        self.depth = view(a.depth, R * cap, torch.int32, (R, cap))
+        self.beam_mask = view(a.beam_mask, R * cap, torch.int32, (R, cap))  # uint32 bits
+        self.leaf = view(a.leaf, R * 32, torch.int32, (R, 32))
+        self.score = view(a.score, R * 32, torch.float32, (R, 32))
+        self.n_nodes = view(a.n_nodes, R, torch.int32, (R,))
+        self.prompt_len = view(a.prompt_len, R, torch.int32, (R,))
+
+    @property
+    def b_live(self) -> int:
+        return L.trie_get_arrays(self.h).b_live
+
+    @property
+    def steps(self) -> int:
+        return L.trie_get_arrays(self.h).steps
+
+    def new_pools(self):
+        """Zero-initialised K and V pools, one [R][Hkv][cap][D] tensor per layer."""
+        shape = (self.L, self.R, self.Hkv, self.cap, self.D)
+        return (torch.zeros(shape, dtype=self.dtype, device=self.device),
+                torch.zeros(shape, dtype=self.dtype, device=self.device))
+
+    # ---- C ABI calls ----------------------------------------------------------------
+    def reset(self, stream=None):
+        L.trie_reset(self.h, stream)
+
+    def rope_kv_append(self, q, k_new, v_new, k_pool_l, v_pool_l, rope_theta, stream=None):
+        L.trie_rope_kv_append(self.h, q, k_new, v_new, k_pool_l, v_pool_l, rope_theta, stream)
+
+    def attn_decode(self, q, k_pool_l, v_pool_l, out, lse=None, rows_hint=0, use_mask=True,
+                    stream=None):
+        b_live = self.b_live
+        need = L.trie_attn_scratch_bytes(self.cfg, b_live, rows_hint)
+        if self.attn_scratch is None or self.attn_scratch.numel() < need:
+            self.attn_scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+        L.trie_attn_decode(self.cfg, b_live, q, k_pool_l, v_pool_l, self.prompt_len, self.parent,
+                           self.depth, self.leaf, self.n_nodes, self.beam_mask if use_mask else None,
+                           self.window, rows_hint, out, lse, self.attn_scratch, stream)
+
+    def beam_step(self, logits, sel_parent=None, sel_token=None, new_score=None, stream=None):
+        L.trie_beam_step(self.h, logits, sel_parent, sel_token, new_score, stream)
+
+    def append(self, sel_parent, sel_token, new_score=None, stream=None):
+        L.trie_append(self.h, sel_parent, sel_token, new_score, stream)
+
+    def prune_compact(self, k_pools, v_pools, stream=None):
+        L.trie_prune_compact(self.h, [k_pools[l] for l in range(self.L)],
+                             [v_pools[l] for l in range(self.L)], stream)
+
+    def read_hyps(self, max_len, stream=None):
+        need = self.R * 32 * (max_len + 1) * 4
+        if self.hyp_scratch is None or self.hyp_scratch.numel() < need:
+            self.hyp_scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return L.trie_read_hyps(self.h, self.R, self.b_live, max_len, self.hyp_scratch, stream)
+
+    def status(self, stream=None) -> int:
+        return L.trie_status(self.h, stream)
+
+    def close(self):
+        if self.h is not None:
+            L.trie_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

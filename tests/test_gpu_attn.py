@@ -1,0 +1,110 @@
+"""GPU vs oracle: trie_attn_decode and trie_rope_kv_append.
+
+Each side builds its own trie from the same seeded selection sequence (GPU: trie_append +
+trie_prune_compact; oracle: build_tries), the integer states are checked equal, then the
+GPU kernel and oracle.kernels_ref.attn_ref run on the same seeded Q/K/V.  Tolerances
+(BASELINE.json north_star, reading R24): 1e-4 relative for fp32, 2e-2 for bf16; lse
+absolute 1e-4 / 2e-2.  Shapes span several tiles, ragged prompt lengths, GQA groups,
+windows, b_live = 1, and the beam_mask == NULL (Alg. 3 walk) variant."""
+import zlib
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle.kernels_ref import attn_ref, build_tries, soa
+from oracle.numerics import rope_rotate_half
+from tests.gpu_util import need_gpu, per_request_selections, rel_err
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # name, R, b, t_max, ragged, steps, rho, Hq, Hkv, D, window, dtype, use_mask
+    ("tiny", 2, 3, 8, False, 16, 0.5, 4, 4, 16, 0, "f32", True),
+    ("tiny-walk", 3, 3, 8, True, 16, 0.5, 4, 2, 16, 0, "f32", False),
+    ("phi-like", 2, 4, 800, False, 12, 0.5, 32, 32, 96, 0, "bf16", True),
+    ("phi-f32", 1, 4, 300, False, 9, 0.3, 8, 8, 96, 0, "f32", True),
+    ("llama-like", 2, 8, 150, True, 40, 0.5, 32, 8, 128, 0, "bf16", True),
+    ("llama-f32", 2, 8, 150, False, 20, 0.5, 8, 2, 128, 0, "f32", True),
+    ("swa", 2, 4, 300, False, 20, 0.5, 8, 2, 128, 64, "bf16", True),
+    ("swa-w1", 1, 4, 50, False, 6, 0.5, 4, 1, 64, 1, "f32", True),
+    ("b32", 1, 32, 500, False, 10, 0.9, 8, 2, 128, 0, "bf16", True),
+    ("b16-g4", 1, 16, 700, False, 8, 0.0, 16, 4, 128, 0, "bf16", True),
+    ("b1", 3, 1, 40, True, 5, 0.0, 4, 4, 32, 0, "f32", True),
+    ("d256", 1, 2, 70, False, 4, 0.5, 2, 1, 256, 0, "f32", True),
+]
+
+
+@pytest.mark.parametrize("name,R,b,t_max,ragged,steps,rho,Hq,Hkv,D,W,dt,use_mask", CASES,
+                         ids=[c[0] for c in CASES])
+def test_attn_matches_oracle(name, R, b, t_max, ragged, steps, rho, Hq, Hkv, D, W, dt, use_mask):
+    need_gpu()
+    from paper_2502_00085_b200.trie import TrieState
+    seed = zlib.crc32(name.encode()) % 1000
+    V = 500
+    lens = synth.ragged_lens(seed, R, t_max) if ragged else None
+    prompts, lens = synth.prompts(seed, R, t_max, V, lens)
+    sels = per_request_selections(seed, R, steps, b, V, rho)
+    cap = t_max + b * steps + b
+    dtype = torch.bfloat16 if dt == "bf16" else torch.float32
+    st = TrieState(R, b, t_max, cap, 1, Hq, Hkv, D, V, prompts, lens, window=W, dtype=dtype)
+    kp0, vp0 = st.new_pools()
+    for k, (par, tok) in enumerate(sels, 1):
+        st.append(torch.as_tensor(par, device="cuda"), torch.as_tensor(tok, device="cuda"))
+        st.prune_compact(kp0, vp0)
+    tries = build_tries(prompts, lens, sels, b, g=1, final_gc=True)
+    ref = soa(tries, cap, b)
+    assert np.array_equal(st.n_nodes.cpu().numpy(), ref["N"])
+    # seeded K/V for every slot and Q for the b leaves, rounded to the kernel's dtype
+    K = synth.normal(seed, 1, (R, Hkv, cap, D))
+    Vv = synth.normal(seed, 2, (R, Hkv, cap, D))
+    Q = synth.normal(seed, 3, (R, b, Hq, D))
+    tK, tV, tQ = (torch.as_tensor(x, dtype=torch.float32).to(dtype).cuda() for x in (K, Vv, Q))
+    K, Vv, Q = (x.float().cpu().numpy().astype(np.float64) for x in (tK, tV, tQ))
+    out = torch.empty_like(tQ)
+    lse = torch.empty(R, b, Hq, dtype=torch.float32, device="cuda")
+    st.attn_decode(tQ, tK, tV, out, lse, rows_hint=int(ref["N"].max()), use_mask=use_mask)
+    torch.cuda.synchronize()
+    o = out.float().cpu().numpy()
+    l = lse.cpu().numpy()
+    tol = 1e-4 if dt == "f32" else 2e-2
+    for r in range(R):
+        N = tries[r].N
+        o_ref, lse_ref = attn_ref(Q[r], K[r][:, :N], Vv[r][:, :N], tries[r], window=W)
+        assert rel_err(o[r], o_ref) <= tol, f"{name} r={r}: rel err {rel_err(o[r], o_ref)}"
+        assert np.abs(l[r] - lse_ref).max() <= tol * max(1.0, np.abs(lse_ref).max())
+    assert st.status() == 0
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_rope_kv_append_matches_oracle(dt):
+    """a-1: RoPE at depth (§3.4) + write-before-read append, vs oracle rope_rotate_half."""
+    need_gpu()
+    from paper_2502_00085_b200.trie import TrieState
+    R, b, t_max, Hq, Hkv, D, V, base = 2, 4, 700, 8, 2, 128, 100, 500000.0
+    prompts, lens = synth.prompts(5, R, t_max, V, [700, 333])
+    dtype = torch.bfloat16 if dt == "bf16" else torch.float32
+    st = TrieState(R, b, t_max, t_max + 20, 1, Hq, Hkv, D, V, prompts, lens, dtype=dtype)
+    sels = per_request_selections(5, R, 2, b, V, 0.5)
+    for par, tok in sels:
+        st.append(torch.as_tensor(par, device="cuda"), torch.as_tensor(tok, device="cuda"))
+    q = torch.as_tensor(synth.normal(6, 1, (R, b, Hq, D)), dtype=torch.float32).to(dtype).cuda()
+    k = torch.as_tensor(synth.normal(6, 2, (R, b, Hkv, D)), dtype=torch.float32).to(dtype).cuda()
+    v = torch.as_tensor(synth.normal(6, 3, (R, b, Hkv, D)), dtype=torch.float32).to(dtype).cuda()
+    q0, k0, v0 = (x.float().cpu().numpy().astype(np.float64) for x in (q, k, v))
+    kp, vp = st.new_pools()
+    st.rope_kv_append(q, k, v, kp[0], vp[0], base)
+    torch.cuda.synchronize()
+    tol = 1e-5 if dt == "f32" else 1e-2
+    leaf = st.leaf.cpu().numpy()
+    depth = st.depth.cpu().numpy()
+    for r in range(R):
+        for j in range(b):
+            pos = int(depth[r, leaf[r, j]])
+            assert pos == int(lens[r]) + 1           # two appends: depth t + 1 (§3.4)
+            qr = rope_rotate_half(q0[r, j], pos, base)
+            kr = rope_rotate_half(k0[r, j], pos, base)
+            assert rel_err(q[r, j].float().cpu().numpy(), qr) <= tol
+            assert rel_err(kp[0, r, :, leaf[r, j]].float().cpu().numpy(), kr) <= tol
+            assert np.array_equal(vp[0, r, :, leaf[r, j]].float().cpu().numpy(), v0[r, j])
