@@ -200,6 +200,10 @@ const char* trie_last_error(void);
 /* library version (major << 16 | minor) */
 int trie_version(void);
 
+/* Number of kernels this process has launched through the library (all entry points;
+ * used by bench.py to report the launches inside its timed region). */
+unsigned long long trie_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

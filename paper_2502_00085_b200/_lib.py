@@ -21,7 +21,7 @@ TRIE_ST_CAPACITY, TRIE_ST_PARENT, TRIE_ST_EMPTY_ROW, TRIE_ST_LEAF = 1, 2, 4, 8
 SYMBOLS = ["trie_workspace_bytes", "trie_create", "trie_reset", "trie_destroy", "trie_get_arrays",
            "trie_rope_kv_append", "trie_attn_scratch_bytes", "trie_attn_decode", "trie_beam_step",
            "trie_append", "trie_prune_compact", "trie_read_hyps", "trie_status", "trie_last_error",
-           "trie_version"]
+           "trie_version", "trie_launch_count"]
 
 
 class trie_cfg(ctypes.Structure):
@@ -67,6 +67,7 @@ def load(path: str = LIB_PATH):
         "trie_status": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_uint32), P]),
         "trie_last_error": (ctypes.c_char_p, []),
         "trie_version": (ctypes.c_int, []),
+        "trie_launch_count": (ctypes.c_ulonglong, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -193,3 +194,7 @@ def trie_version() -> int:
 
 def trie_last_error() -> str:
     return load().trie_last_error().decode()
+
+
+def trie_launch_count() -> int:
+    return int(load().trie_launch_count())

@@ -4,6 +4,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
 #include <new>
 
 #include "attn_common.cuh"
@@ -11,6 +12,7 @@
 #include "handle.h"
 
 static thread_local char g_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
 
 int trie_set_error(int code, const char* fmt, ...) {
   va_list ap;
@@ -21,6 +23,7 @@ int trie_set_error(int code, const char* fmt, ...) {
 }
 
 int trie_check_launch(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);  // one call per kernel launch site
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return trie_set_error(TRIE_ECUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -108,6 +111,8 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
 extern "C" {
 
 int trie_version(void) { return (1 << 16) | 0; }
+
+unsigned long long trie_launch_count(void) { return g_launches.load(); }
 
 const char* trie_last_error(void) { return g_err; }
 
