@@ -126,7 +126,7 @@ def run_gpu(args):
     if args.requests:
         wl["R"] = args.requests
     L, Hq, Hkv, D, V, t, b, s, R, W = (wl[k] for k in ("L", "Hq", "Hkv", "D", "V", "t", "b", "s", "R", "W"))
-    cap = t + b * s + b
+    cap = (t + b * s + b + 63) // 64 * 64  # whole 64-slot tiles (the TMA path needs cap % 4 == 0)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     import synth
@@ -244,8 +244,8 @@ def run_gpu(args):
                config=dict(workload=wl["name"], requests_per_gpu=R, beam=b, prompt_len=t,
                            new_tokens=s, layers=L, q_heads=Hq, kv_heads=Hkv, head_dim=D, vocab=V,
                            window=W, gc_interval=1, parallelism=f"request-dp{world}",
-                           l2="per-layer KV read > L2 (no flush needed)" if R * t * Hkv * D * 4 > 126e6
-                           else "inputs smaller than L2"))
+                           l2=(f"no flush: each layer's pool is re-read once per step and the "
+                               f"per-step KV footprint ({R * t * Hkv * D * 4 * L / 1e6:.0f} MB) > L2 (126 MB)")))
     res["roofline"] = dict(kernel="trie_attn_decode", bound="hbm", achieved=round(ach, 1), peak=peak,
                            unit="GB/s", frac=round(ach / peak, 4), frac_of_8TBps=round(ach / 8000, 4),
                            traffic=None, peak_source=peak_src,
@@ -253,13 +253,17 @@ def run_gpu(args):
                            attn_share_of_step=round(float(np.sum(attn_ms)) / ms, 4))
     res["clocks"] = clk
     res["gpu_launches"] = int(launches)
-    # KV memory vs batch beam search (logical bytes), at the final measured step
-    n_last = nh[-1]
+    # KV memory vs batch beam search (logical bytes, SURVEY reading A18) at the timed step
+    # that is deepest into its job: batch holds b * (t + k) rows per request (prompt
+    # replicated, pending tokens included, P:42 counting); the trie holds N rows.
+    i_star = int(np.argmax(k_hist))
+    k_star = k_hist[i_star]
     kv_row = L * 2 * Hkv * D * 2
-    trie_b = int(n_last.sum()) * kv_row
-    batch_b = R * b * (t + s) * kv_row
-    res["kv_memory"] = dict(trie_bytes_last_step=trie_b, batch_bytes_full_len=batch_b,
-                            ratio_batch_over_trie=round(batch_b / max(trie_b, 1), 3))
+    trie_b = int(nh[i_star].sum()) * kv_row
+    batch_b = R * (b if k_star > 0 else 1) * (t + k_star) * kv_row
+    res["kv_memory"] = dict(step_in_job=int(k_star), trie_bytes=trie_b, batch_bytes=batch_b,
+                            ratio_batch_over_trie=round(batch_b / max(trie_b, 1), 3),
+                            bound_b_ts_over_t_s_b_1=round(b * (t + k_star) / (t + k_star + b - 1), 3))
     return res, dict(st=st, kp=kp, vp=vp, qkv=qkv, logits=logits, L=L, R=R, b=b, s=s, t=t, V=V,
                      world=world, rank=rank, dev=dev, wl=wl)
 

@@ -283,6 +283,7 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
   p.splits = splits;
   p.scale_log2 = 1.4426950408889634f / sqrtf((float)cfg->head_dim);
   p.bf16 = cfg->kv_dtype == TRIE_BF16;
+  if (trie::attn_tc_supported(p)) return trie::launch_attn_tc(p, stream);
   return trie::launch_attn_v1(p, stream);
 }
 

@@ -23,7 +23,8 @@ struct AttnParams {
 };
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);
-int launch_attn_tc(const AttnParams& p, cudaStream_t s);  // returns 1 if shape unsupported
-size_t attn_tc_part_bytes(const AttnParams& p);
+int launch_attn_tc(const AttnParams& p, cudaStream_t s);
+bool attn_tc_supported(const AttnParams& p);
+int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s);
 
 }  // namespace trie

@@ -245,6 +245,13 @@ static int launch_v1_t(const AttnParams& p, cudaStream_t s) {
   return rc;
 }
 
+int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s) {
+  const int Qg = p.b_live * (p.Hq / p.Hkv);
+  const int warps = p.R * p.Hkv * Qg;
+  k_attn_combine<__nv_bfloat16><<<(warps * 32 + 255) / 256, 256, 0, s>>>(p);
+  return trie_check_launch("k_attn_combine");
+}
+
 int launch_attn_v1(const AttnParams& p, cudaStream_t s) {
   return p.bf16 ? launch_v1_t<__nv_bfloat16>(p, s) : launch_v1_t<float>(p, s);
 }
