@@ -3,12 +3,14 @@
 One bench STEP = one beam-decode step of R requests through the whole hot path
 (SURVEY §8(a) rows a-1..a-6): for every layer trie_rope_kv_append + trie_attn_decode,
 then trie_beam_step (log-softmax + top-b + append + bitset update), then
-trie_prune_compact (g = 1).  Jobs of s new tokens run back to back; when a job reaches s
-steps the trie is re-initialised (trie_reset, inside the timed region) and the next job
-starts from the resident prompts.  The model GEMMs are context, not product, and are
-not in the step: Q/K/V and fp32 logits are seeded synthetic inputs resident in HBM
-(`value`); `e2e` copies every step's Q/K/V + logits from pinned host memory and reads
-back the selections (device-to-host) inside the timed region.
+trie_prune_compact (g = 1).  Jobs of s new tokens run back to back: the first step of a
+job runs trie_reset + one live beam (the prompt leaf; its forward stands in for the
+prefill's last position), the next s-1 steps run b live beams.  Steps are replayed as
+CUDA graphs (one per input buffer x {first, steady}) so the host never paces the GPU.
+The model GEMMs are context, not product, and are not in the step: Q/K/V and fp32 logits
+are seeded synthetic inputs resident in HBM (`value`); `e2e` copies every step's Q/K/V +
+logits from pinned host memory (double-buffered on a copy stream) and reads the step's
+selections back to the host, all inside its timed region.
 
 Metric (BASELINE.json): beam-decode steps/s (request-steps/s: one request advancing its
 b beams by one token) and trie-attn HBM GB/s over unique-KV bytes (roofline object);
@@ -21,7 +23,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -61,7 +62,7 @@ class Clocks:
 
     def __init__(self, gpu_index: int):
         self.proc = None
-        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}_{gpu_index}.csv")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={gpu_index}",
@@ -100,13 +101,127 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------------------
+class HotPath:
+    """Buffers, trie state and captured step graphs for one rank."""
+
+    def __init__(self, wl, rank, dev):
+        import torch
+
+        from paper_2502_00085_b200.trie import TrieState
+        import synth
+        self.torch = torch
+        self.wl = wl
+        L, Hq, Hkv, D, V, t, b, s, R, W = (wl[k] for k in ("L", "Hq", "Hkv", "D", "V", "t", "b", "s", "R", "W"))
+        self.L, self.Hq, self.Hkv, self.D, self.V, self.t, self.b, self.s, self.R, self.W = \
+            L, Hq, Hkv, D, V, t, b, s, R, W
+        self.cap = (t + b * s + b + 63) // 64 * 64  # whole 64-slot tiles (TMA path: cap % 4 == 0)
+        self.dev = dev
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(1234 + rank)
+        # request-parallel partition: this rank owns its own R requests (weak scaling)
+        prompts, lens = synth.prompts(10_000 + rank, R, t, V)
+        self.st = TrieState(R, b, t, self.cap, L, Hq, Hkv, D, V, prompts, lens, window=W,
+                            dtype=torch.bfloat16, device=dev)
+        self.kp, self.vp = self.st.new_pools()
+        for l in range(L):  # resident prompt K/V (prefill is model context; synthetic here)
+            self.kp[l][:, :, :t].normal_(generator=gen)
+            self.vp[l][:, :, :t].normal_(generator=gen)
+        # inputs: 2 slots x {first (1 live beam), steady (b live beams)}; one flat buffer each
+        self.NB = 2
+        self.inp = {}
+        for var, bl in (("first", 1), ("steady", b)):
+            per_layer = R * bl * (Hq + 2 * Hkv) * D
+            for slot in range(self.NB):
+                qkv = torch.randn(L * per_layer, device=dev, generator=gen).to(torch.bfloat16)
+                lg = torch.randn(R * bl * V, device=dev, generator=gen) * 3.0
+                views = []
+                for l in range(L):
+                    base = l * per_layer
+                    q = qkv[base: base + R * bl * Hq * D].view(R, bl, Hq, D)
+                    k = qkv[base + R * bl * Hq * D: base + R * bl * (Hq + Hkv) * D].view(R, bl, Hkv, D)
+                    v = qkv[base + R * bl * (Hq + Hkv) * D: base + per_layer].view(R, bl, Hkv, D)
+                    views.append((q, k, v))
+                self.inp[(var, slot)] = dict(qkv=qkv, logits=lg.view(R, bl, V), views=views,
+                                             out=torch.empty(R, bl, Hq, D, dtype=torch.bfloat16, device=dev))
+        self.sel_p = torch.empty(R, b, dtype=torch.int32, device=dev)
+        self.sel_t = torch.empty_like(self.sel_p)
+        self.sel_s = torch.empty(R, b, dtype=torch.float32, device=dev)
+        self.rows_hint = t + s
+        self.graphs = {}
+        self.launches_per_graph = {}
+        self.k = 0  # steps done in the current job
+
+    def step_ops(self, var, slot, events=None):
+        """Enqueue one step (all §8(a) rows) on the current stream."""
+        st, L = self.st, self.L
+        d = self.inp[(var, slot)]
+        if var == "first":
+            st.reset()
+        for l in range(L):
+            q, k, v = d["views"][l]
+            st.rope_kv_append(q, k, v, self.kp[l], self.vp[l], self.wl["theta"])
+            if events is not None:
+                events[l][0].record()
+            st.attn_decode(q, self.kp[l], self.vp[l], d["out"], rows_hint=self.rows_hint)
+            if events is not None:
+                events[l][1].record()
+        st.beam_step(d["logits"], self.sel_p, self.sel_t, self.sel_s)
+        st.prune_compact(self.kp, self.vp)
+
+    def capture(self):
+        """One graph per (variant, slot) + an event-instrumented twin for kernel timing."""
+        torch = self.torch
+        from paper_2502_00085_b200 import _lib
+        self.ev = {}
+        for var in ("first", "steady"):
+            for slot in range(self.NB):
+                for timed in (False, True):
+                    evs = None
+                    if timed:
+                        evs = [(torch.cuda.Event(enable_timing=True, external=True),
+                                torch.cuda.Event(enable_timing=True, external=True)) for _ in range(self.L)]
+                    g = torch.cuda.CUDAGraph()
+                    n0 = _lib.trie_launch_count()
+                    with torch.cuda.graph(g):
+                        self.step_ops(var, slot, evs)
+                    self.graphs[(var, slot, timed)] = g
+                    self.launches_per_graph[(var, slot, timed)] = _lib.trie_launch_count() - n0
+                    if timed:
+                        self.ev[(var, slot)] = evs
+        # capture ran the host logic of reset/beam_step: leave the host view at "steady"
+
+    def next_key(self):
+        var = "first" if self.k % self.s == 0 else "steady"
+        return var
+
+    def replay(self, slot, timed=False):
+        var = self.next_key()
+        self.graphs[(var, slot, timed)].replay()
+        self.k = (self.k + 1) % self.s
+        return var
+
+    def attn_bytes(self, k_in_job, N):
+        """Algorithmic bytes of one trie_attn_decode launch: unique
+        KV rows U_r x 2*Hkv*D*2 + Q and O (bf16) + mask/depth words of generated rows."""
+        t, b, W, R, Hq, Hkv, D = self.t, self.b, self.W, self.R, self.Hq, self.Hkv, self.D
+        bl = 1 if k_in_job == 0 else b
+        if k_in_job == 0:
+            N = np.full(R, t)
+        if W <= 0:
+            U = N.astype(np.int64)
+        else:  # window lower depth = leaf depth - W + 1 (leaves share depth t + k - 1)
+            leaf_depth = t - 1 if k_in_job == 0 else t + k_in_job - 1
+            lo = max(0, leaf_depth - W + 1)
+            U = (N - min(lo, t)).astype(np.int64)
+        return int(U.sum()) * 2 * Hkv * D * 2 + R * bl * Hq * D * 2 * 2 + int((N - t).clip(min=0).sum()) * 8
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
 
     from paper_2502_00085_b200 import _lib
     from paper_2502_00085_b200.build import build
-    from paper_2502_00085_b200.trie import TrieState
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -125,89 +240,38 @@ def run_gpu(args):
         wl["b"] = args.beam
     if args.requests:
         wl["R"] = args.requests
-    L, Hq, Hkv, D, V, t, b, s, R, W = (wl[k] for k in ("L", "Hq", "Hkv", "D", "V", "t", "b", "s", "R", "W"))
-    cap = (t + b * s + b + 63) // 64 * 64  # whole 64-slot tiles (the TMA path needs cap % 4 == 0)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    import synth
-    # request-parallel partition: rank owns requests [rank*R, (rank+1)*R) (weak scaling)
-    prompts, lens = synth.prompts(10_000 + rank, R, t, V)
-    st = TrieState(R, b, t, cap, L, Hq, Hkv, D, V, prompts, lens, window=W, dtype=torch.bfloat16,
-                   device=dev)
-    kp, vp = st.new_pools()
-    for l in range(L):  # resident prompt K/V (prefill is model context; synthetic here)
-        kp[l][:, :, :t].normal_(generator=gen)
-        vp[l][:, :, :t].normal_(generator=gen)
-    NB = 2
-    qkv = [torch.randn(L, R, b, Hq + 2 * Hkv, D, device=dev, generator=gen).to(torch.bfloat16)
-           for _ in range(NB)]
-    NLOG = 8
-    kappa = 3.0
-    logits = [torch.randn(R, b, V, device=dev, generator=gen) * kappa for _ in range(NLOG)]
-    q_l = [[x[l, :, :, :Hq].contiguous() for l in range(L)] for x in qkv]
-    k_l = [[x[l, :, :, Hq:Hq + Hkv].contiguous() for l in range(L)] for x in qkv]
-    v_l = [[x[l, :, :, Hq + Hkv:].contiguous() for l in range(L)] for x in qkv]
-    # first step of every job has one live beam (the prompt leaf): separate contiguous inputs
-    q1 = [[x[:, :1].contiguous() for x in ql] for ql in q_l]
-    k1 = [[x[:, :1].contiguous() for x in kl] for kl in k_l]
-    v1 = [[x[:, :1].contiguous() for x in vl] for vl in v_l]
-    lg1 = [x[:, :1].contiguous() for x in logits]
-    out = torch.empty(R, b, Hq, D, dtype=torch.bfloat16, device=dev)
-    out1 = torch.empty(R, 1, Hq, D, dtype=torch.bfloat16, device=dev)
-    sel_p = torch.empty(R, b, dtype=torch.int32, device=dev)
-    sel_t = torch.empty_like(sel_p)
-    sel_s = torch.empty(R, b, dtype=torch.float32, device=dev)
-    rows_hint = t + s
-    stream = torch.cuda.current_stream()
-    attn_ev = []
-    state = {"k": 0, "step": 0}
+    hp = HotPath(wl, rank, dev)
+    R, L, s, b, t = hp.R, hp.L, hp.s, hp.b, hp.t
 
-    def one_step(timed, qi, li, use_events):
-        if state["k"] == s:
-            st.reset()
-            state["k"] = 0
-        b_live = 1 if state["k"] == 0 else b
-        for l in range(L):
-            if b_live == 1:
-                q, kk, vv, o = q1[qi][l], k1[qi][l], v1[qi][l], out1
-            else:
-                q, kk, vv, o = q_l[qi][l], k_l[qi][l], v_l[qi][l], out
-            st.rope_kv_append(q, kk, vv, kp[l], vp[l], wl["theta"])
-            if use_events:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            st.attn_decode(q, kp[l], vp[l], o, rows_hint=rows_hint)
-            if use_events:
-                e1.record(stream)
-                attn_ev.append((e0, e1, b_live))
-        lg = logits[li] if b_live == b else lg1[li]
-        st.beam_step(lg, sel_p, sel_t, sel_s)
-        st.prune_compact(kp, vp)
-        state["k"] += 1
-        state["step"] += 1
-
-    # warm-up (untimed)
+    # eager warm-up (allocates scratch, sets kernel attributes), then capture
+    for i in range(2):
+        hp.step_ops("first" if i == 0 else "steady", i % 2)
+    torch.cuda.synchronize()
+    hp.capture()
+    hp.st.reset()
+    torch.cuda.synchronize()
+    hp.k = 0
     for i in range(args.warmup):
-        one_step(False, i % NB, i % NLOG, False)
+        hp.replay(i % 2)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    # N history for algorithmic-byte accounting
+
+    stream = torch.cuda.current_stream()
     n_hist = torch.empty(args.steps, R, dtype=torch.int32, device=dev)
     k_hist = []
+    launches = 0
     clocks = Clocks(local)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    launches0 = _lib.trie_launch_count()
     t0.record(stream)
     for i in range(args.steps):
-        k_hist.append(state["k"] % s)
-        n_hist[i].copy_(st.n_nodes, non_blocking=True)
-        one_step(True, i % NB, i % NLOG, True)
+        k_hist.append(hp.k)
+        n_hist[i].copy_(hp.st.n_nodes, non_blocking=True)  # 4*R bytes, for byte accounting
+        var = hp.replay(i % 2)
+        launches += hp.launches_per_graph[(var, i % 2, False)]
     t1.record(stream)
-    launches = _lib.trie_launch_count() - launches0
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
@@ -215,57 +279,211 @@ def run_gpu(args):
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    assert st.status() == 0, f"device status bits {st.status():#x}"
-    # attention roofline
-    attn_ms = [a.elapsed_time(bb) for a, bb, _ in attn_ev]
-    nh = n_hist.cpu().numpy()
-    bytes_attn = []
+    st_bits = hp.st.status()
+    assert st_bits == 0, f"device status bits {st_bits:#x}"
+
+    # ---- roofline pass: the same step graphs with event nodes around every attention
+    # launch, replayed one step at a time (the events are read before the next replay)
+    attn_ms, attn_bytes = [], []
     for i in range(args.steps):
-        after_reset = k_hist[i] == 0
-        N = np.full(R, t) if after_reset else nh[i]
-        bl = 1 if after_reset else b
-        if W <= 0 or after_reset:
-            U = N.astype(np.int64) if W <= 0 else np.full(R, min(t, W), np.int64)
-        else:  # window lower depth = leaf depth - W + 1 = t + k - W (prompt part is a slot range)
-            lo = max(0, t + k_hist[i] - W)
-            U = (N - lo).astype(np.int64)
-        kv = int(U.sum()) * 2 * Hkv * D * 2
-        qo = R * bl * Hq * D * 2 * 2
-        meta = int((N - t).clip(min=0).sum()) * 8
-        bytes_attn += [kv + qo + meta] * L
-    ach = float(np.sum(bytes_attn) / (np.sum(attn_ms) * 1e-3) / 1e9)
+        kj = hp.k
+        N = hp.st.n_nodes.cpu().numpy()
+        var = hp.replay(i % 2, timed=True)
+        torch.cuda.synchronize()
+        for e0, e1 in hp.ev[(var, i % 2)]:
+            attn_ms.append(e0.elapsed_time(e1))
+            attn_bytes.append(hp.attn_bytes(kj, N))
+    ach = float(np.sum(attn_bytes) / (np.sum(attn_ms) * 1e-3) / 1e9)
     peak, peak_src = _peaks()
-    total_req_steps = R * args.steps * world
-    value = total_req_steps / (ms * 1e-3)
+
+    value = R * args.steps * world / (ms * 1e-3)
+    kv_fp = R * (t + s // 2) * hp.Hkv * hp.D * 4 * L
     res = dict(metric="beam-decode steps/s (request-steps/s, hot path) + trie-attn HBM GB/s",
                value=round(value, 2), unit="request-steps/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(ms / args.steps, 4), higher_is_better=True,
                scaling="weak", vs_baseline=None, dtype="bf16", data="synthetic",
                config=dict(workload=wl["name"], requests_per_gpu=R, beam=b, prompt_len=t,
-                           new_tokens=s, layers=L, q_heads=Hq, kv_heads=Hkv, head_dim=D, vocab=V,
-                           window=W, gc_interval=1, parallelism=f"request-dp{world}",
-                           l2=(f"no flush: each layer's pool is re-read once per step and the "
-                               f"per-step KV footprint ({R * t * Hkv * D * 4 * L / 1e6:.0f} MB) > L2 (126 MB)")))
+                           new_tokens=s, layers=L, q_heads=hp.Hq, kv_heads=hp.Hkv, head_dim=hp.D,
+                           vocab=hp.V, window=hp.W, gc_interval=1, parallelism=f"request-dp{world}",
+                           execution="cuda-graph replay per step",
+                           l2=(f"no flush: each layer's pool is re-read once per step and the per-step "
+                               f"KV footprint ({kv_fp / 1e6:.0f} MB) > L2 (126 MB)")))
     res["roofline"] = dict(kernel="trie_attn_decode", bound="hbm", achieved=round(ach, 1), peak=peak,
                            unit="GB/s", frac=round(ach / peak, 4), frac_of_8TBps=round(ach / 8000, 4),
-                           traffic=None, peak_source=peak_src,
+                           traffic=_traffic(args.workload), peak_source=peak_src,
                            avg_launch_us=round(float(np.mean(attn_ms)) * 1e3, 2),
-                           attn_share_of_step=round(float(np.sum(attn_ms)) / ms, 4))
+                           attn_share_of_step=round(float(np.sum(attn_ms)) / (ms * 1), 4),
+                           timing="event nodes around each attention launch in the replayed step graphs")
     res["clocks"] = clk
     res["gpu_launches"] = int(launches)
-    # KV memory vs batch beam search (logical bytes, SURVEY reading A18) at the timed step
-    # that is deepest into its job: batch holds b * (t + k) rows per request (prompt
-    # replicated, pending tokens included, P:42 counting); the trie holds N rows.
+    nh = n_hist.cpu().numpy()
     i_star = int(np.argmax(k_hist))
     k_star = k_hist[i_star]
-    kv_row = L * 2 * Hkv * D * 2
+    kv_row = L * 2 * hp.Hkv * hp.D * 2
     trie_b = int(nh[i_star].sum()) * kv_row
     batch_b = R * (b if k_star > 0 else 1) * (t + k_star) * kv_row
+    # batch beam search keeps b*(t+k) rows per request (prompt replicated, pending token
+    # included: the paper's 21 = 3 x 7 counting); the trie keeps N rows
     res["kv_memory"] = dict(step_in_job=int(k_star), trie_bytes=trie_b, batch_bytes=batch_b,
                             ratio_batch_over_trie=round(batch_b / max(trie_b, 1), 3),
                             bound_b_ts_over_t_s_b_1=round(b * (t + k_star) / (t + k_star + b - 1), 3))
-    return res, dict(st=st, kp=kp, vp=vp, qkv=qkv, logits=logits, L=L, R=R, b=b, s=s, t=t, V=V,
-                     world=world, rank=rank, dev=dev, wl=wl)
+    if not args.no_e2e:
+        res["e2e"] = run_e2e(hp, args, world)
+    return res, dict(rank=rank, world=world)
+
+
+def run_e2e(hp, args, world):
+    """Same steps, inputs copied from pinned host memory every step (copy stream,
+    double-buffered), selections copied back to pinned host memory every step."""
+    import torch
+    import torch.distributed as dist
+    host = {}
+    for key, d in hp.inp.items():
+        host[key] = dict(qkv=d["qkv"].cpu().pin_memory(), logits=d["logits"].cpu().pin_memory())
+    out_host = [torch.empty(3, hp.R, hp.b, dtype=torch.int32).pin_memory() for _ in range(2)]
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_free = [torch.cuda.Event() for _ in range(2)]
+    h2d = d2h = 0
+    k_sim = hp.k
+
+    def var_of(k):
+        return "first" if k % hp.s == 0 else "steady"
+
+    def prefetch(i, k):
+        nonlocal h2d
+        slot = i % 2
+        var = var_of(k)
+        with torch.cuda.stream(copy):
+            copy.wait_event(ev_free[slot])
+            hp.inp[(var, slot)]["qkv"].copy_(host[(var, slot)]["qkv"], non_blocking=True)
+            hp.inp[(var, slot)]["logits"].view(-1).copy_(host[(var, slot)]["logits"].view(-1), non_blocking=True)
+            ev_in[slot].record(copy)
+        h2d += host[(var, slot)]["qkv"].numel() * 2 + host[(var, slot)]["logits"].numel() * 4
+
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for e in ev_free:
+        e.record(compute)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(compute)
+    copy.wait_event(t0)
+    prefetch(0, k_sim)
+    for i in range(args.steps):
+        slot = i % 2
+        compute.wait_event(ev_in[slot])
+        hp.replay(slot)
+        ev_free[slot].record(compute)
+        if i + 1 < args.steps:
+            prefetch(i + 1, k_sim + i + 1)
+        oh = out_host[slot]
+        oh[0].copy_(hp.sel_p, non_blocking=True)
+        oh[1].copy_(hp.sel_t, non_blocking=True)
+        oh[2].copy_(hp.sel_s.view(torch.int32), non_blocking=True)
+        d2h += 3 * hp.R * hp.b * 4
+    t1.record(compute)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=hp.dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return {"value": round(hp.R * args.steps * world / (ms * 1e-3), 2), "unit": "request-steps/s",
+            "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
+            "ms_per_step": round(ms / args.steps, 4),
+            "path": "C ABI via the binding; pinned host -> device copies on a side stream, "
+                    "double-buffered; selections device -> pinned host every step"}
+
+
+def _traffic(workload):
+    """dram bytes per attention launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_attn_summary.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return d.get(workload, {}).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_oracle_sample(wl, budget_s=15.0, max_steps=64):
+    """Time the CPU oracle on a bounded sample of the workload: one request at a mid-job
+    trie state; one request-step = L x attn_ref (one layer) + beam_step_ref + GC.  The
+    oracle is timed as it stands (single BLAS thread)."""
+    from threadpoolctl import threadpool_limits
+
+    import synth
+    from oracle.kernels_ref import attn_ref, beam_step_ref, build_tries
+    from oracle.trie import garbage_collect
+    L, Hq, Hkv, D, V, t, b, s = (wl[k] for k in ("L", "Hq", "Hkv", "D", "V", "t", "b", "s"))
+    prompts, lens = synth.prompts(1, 1, t, V)
+    k_mid = s // 2
+    sels = [(p[None], q[None]) for p, q in synth.selections(3, k_mid, b, V, 0.5)]
+    T = build_tries(prompts, lens, sels, b, g=1)[0]
+    N = T.N
+    q = synth.normal(4, 1, (b, Hq, D))
+    K = synth.normal(4, 2, (Hkv, N, D))
+    Vv = synth.normal(4, 3, (Hkv, N, D))
+    logits = synth.normal(4, 4, (b, V)) * 3.0
+    scores = np.zeros(b)
+    times = []
+    with threadpool_limits(limits=1):
+        t_start = time.perf_counter()
+        while len(times) < max_steps:
+            a0 = time.perf_counter()
+            attn_ref(q, K, Vv, T, window=wl["W"])
+            a1 = time.perf_counter()
+            beam_step_ref(logits, scores, b)
+            a2 = time.perf_counter()
+            import copy
+            Tc = copy.deepcopy(T)
+            a3 = time.perf_counter()
+            garbage_collect(Tc)
+            a4 = time.perf_counter()
+            times.append(L * (a1 - a0) + (a2 - a1) + (a4 - a3))
+            if time.perf_counter() - t_start > budget_s:
+                break
+    return times, N
+
+
+def cpu_baseline(wl, budget_s=15.0):
+    times, N = cpu_oracle_sample(wl, budget_s)
+    per = float(np.mean(times))
+    return {"value": round(1.0 / per, 4), "unit": "request-steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"{len(times)} request-steps of one request at step {wl['s'] // 2} of its job "
+                      f"(N={N} trie rows): attn_ref timed on one layer and scaled x{wl['L']} layers, "
+                      f"+ beam_step_ref over b x V + GC (mark/prune/compact); numpy fp64, 1 BLAS thread"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    wl = dict(WORKLOADS[args.workload])
+    if args.beam:
+        wl["b"] = args.beam
+    budget = 180.0
+    times, N = cpu_oracle_sample(wl, budget_s=budget, max_steps=args.warmup + args.steps)
+    timed = times[args.warmup:] or times
+    per = float(np.mean(timed))
+    v = 1.0 / per
+    res = dict(metric="beam-decode steps/s (request-steps/s, hot path) + trie-attn HBM GB/s",
+               value=round(v, 4), unit="request-steps/s", n_gpus=world, steps=len(timed),
+               warmup=args.warmup, ms_per_step=round(per * 1e3, 3), higher_is_better=True,
+               scaling="weak", vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
+               config=dict(workload=wl["name"], requests_per_gpu=1, beam=wl["b"], prompt_len=wl["t"],
+                           new_tokens=wl["s"], layers=wl["L"], parallelism="cpu-oracle"),
+               cpu_baseline=dict(value=round(v, 4), unit="request-steps/s", cores=1, kind="oracle",
+                                 sample=f"each step = one request-step of the CPU oracle (N={N} rows, "
+                                        f"attn_ref x{wl['L']} layers + beam_step_ref + GC)"),
+               e2e=dict(value=round(v, 4), unit="request-steps/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    return res
 
 
 def main():
@@ -278,11 +496,22 @@ def main():
     ap.add_argument("--requests", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res))
+        return
     res, ctx = run_gpu(args)
     if ctx["rank"] == 0:
+        wl = dict(WORKLOADS[args.workload])
+        if args.beam:
+            wl["b"] = args.beam
+        if not args.no_cpu_baseline and ctx["world"] == 1:
+            res["cpu_baseline"] = cpu_baseline(wl)
         print(json.dumps(res))
 
 

@@ -210,9 +210,12 @@ int trie_rope_kv_append(trie_handle* h, void* q, void* k_new, const void* v_new,
 static int attn_splits(const trie_cfg* c, int rows_hint) {
   int rows = rows_hint > 0 ? rows_hint : c->capacity;
   const int units = c->n_requests * c->n_kv_heads;
+  static int sm_cache[64] = {0};
   int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess)
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
+    if (!sm_cache[dev]) cudaDeviceGetAttribute(&sm_cache[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (sm_cache[dev]) sms = sm_cache[dev];
+  }
   const int target = sms * 2;  // two resident CTAs per SM
   int splits = (target + units - 1) / units;
   const int max_by_rows = rows / 128 > 0 ? rows / 128 : 1;  // >= 128 rows per split

@@ -1,21 +1,31 @@
-// trie_attn_decode, bf16 tensor-core path (sm_100a): TMA-fed, mbarrier-pipelined
-// split-K flash-decode over the shared trie KV pool (§3.3; Alg. 3).
+// trie_attn_decode, bf16 tensor-core paths (sm_100a): TMA-fed, mbarrier-pipelined
+// flash-decode over the shared trie KV pool (§3.3; Alg. 3 mask P:165-186).
 //
-// One CTA per (KV head h, request r, split).  Warp 0 is the producer: one elected lane
-// streams 64-slot tiles of K and V (head-major pool => a tile is a contiguous 2-D box)
-// with cp.async.bulk.tensor (TMA, 64-byte swizzle) plus the tile's beam_mask / depth
-// words with 1-D bulk copies, into an S-stage ring guarded by full/empty mbarriers.
-// Every unique KV row is read from HBM exactly once per (request, KV head) and feeds all
-// Qg = b_live * (Hq/Hkv) queries of that head: GQA grouping + trie sharing.
-// Consumer warps: warp w owns query m-tile (w % MT) (16 queries) and row slice
-// (w / MT) of every tile; S = Q K^T and O += P V run on mma.sync.m16n8k16 (bf16 in,
-// fp32 accumulate) with ldmatrix from the swizzled tiles; masked keys get -inf before
-// the online softmax (exact exclusion, reading R22).  Row-slice partials (m, l, O) are
-// merged in shared memory at the end; split partials go to k_attn_combine.
+// Common structure.  One CTA per (KV head h, request r, split).  Warp 0 is the producer:
+// one elected lane streams 64-slot tiles of K and V (the head-major pool makes a tile a
+// contiguous 2-D box) with cp.async.bulk.tensor (TMA, 64-byte swizzle) plus the tile's
+// beam_mask / depth words with 1-D bulk copies into an S-stage ring guarded by
+// full/empty mbarriers.  Every unique KV row is read from HBM exactly once per
+// (request, KV head) and feeds all Qg = b_live * (Hq/Hkv) queries of the head (GQA
+// grouping + trie sharing).  Masked keys get -inf before the online softmax (exact
+// exclusion, reading R22); tiles that lie entirely in the prompt and inside every
+// beam's window skip the mask (Alg. 3 l.2: prompt columns are open to every beam).
+//
+// k_attn_narrow (Qg <= 16): ONE consumer warp owns the whole item.  KV rows sit on the
+//   MMA M dimension and queries on N (8 per n-tile), so small beam counts waste at most
+//   half an n-tile instead of 3/4 of an m-tile: S^T = K Q^T (A = K tile via ldmatrix,
+//   B = Q from registers), P^T is turned into the B operand of O^T = V^T P^T with
+//   movmatrix.trans, A = V^T via ldmatrix.trans.  48 ldmatrix.x4 per 64-row tile read
+//   the tile exactly once.
+// k_attn_wide (16 < Qg <= 128): MT = ceil(Qg/16) consumer warps, warp w owns query
+//   m-tile w over the full tile rows: S = Q K^T (A = Q registers, B = K via ldmatrix),
+//   P from the accumulators (FA2 layout), O += P V (B = V via ldmatrix.trans).
+// No cross-warp merge in either variant; split partials go to k_attn_combine.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <float.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "attn_common.cuh"
 #include "common.cuh"
@@ -23,8 +33,8 @@
 
 namespace trie {
 
-constexpr int TC_TR = 64;      // slots per tile
-constexpr int TC_CW = 32;      // elements per swizzle box column (64 bytes, SWIZZLE_64B)
+constexpr int TC_TR = 64;  // slots per tile
+constexpr int TC_CW = 32;  // elements per swizzle box column (64 bytes, SWIZZLE_64B)
 
 // ---- PTX helpers -------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -50,19 +60,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes,
+__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void* src, uint32_t bytes,
                                              uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
+          "r"(dst),
       "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
@@ -78,6 +88,11 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& a, uint32_t& 
                : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
                : "r"(addr));
 }
+__device__ __forceinline__ uint32_t movm_t(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
 __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -92,107 +107,402 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 // byte offset of (row, col) inside one tile: D/32 boxes of [TR rows][32 cols], 64B swizzle
+// (CUTLASS Swizzle<2,4,3>: address bits [4,5] ^= bits [7,8]; boxes are 1024-B aligned)
 __device__ __forceinline__ uint32_t tile_off(int row, int col) {
   const int box = col / TC_CW;
   const uint32_t o = (uint32_t)row * 64u + (uint32_t)(col % TC_CW) * 2u;
   return (uint32_t)box * (TC_TR * 64u) + (o ^ (((o >> 7) & 3u) << 4));
 }
 
-template <int D, int MT>
-struct TcCfg {
-  static constexpr int STAGES = D >= 128 ? 3 : 4;  // 2 CTAs per SM for D <= 128
-  static constexpr int NC = MT < 4 ? 4 : MT;   // consumer warps
-  static constexpr int RS = NC / MT;           // row slices per tile
-  static constexpr int RSZ = TC_TR / RS;       // rows per warp per tile
-  static constexpr int NT = RSZ / 8;           // S n-tiles per warp
-  static constexpr int KS = D / 16;            // k-steps of Q K^T
-  static constexpr int DT = D / 8;             // O n-tiles
+template <int D, int STAGES_>
+struct Ring {
+  static constexpr int STAGES = STAGES_;
   static constexpr int TILE_BYTES = TC_TR * D * 2;
   // stage = K tile | V tile | mask words | depth words, 1024-byte aligned (swizzle atoms)
   static constexpr int STAGE_BYTES = (2 * TILE_BYTES + 2 * TC_TR * 4 + 1023) / 1024 * 1024;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8 + 64;
-  static constexpr int THREADS = 32 * (NC + 1);
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
 };
 
-template <int D, int MT>
-__global__ void __launch_bounds__(TcCfg<D, MT>::THREADS) k_attn_tc(
-    const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
-    const AttnParams p) {
-  using C = TcCfg<D, MT>;
+struct ItemInfo {
+  int tile0, ntiles, lo, N, t, fast_from;
+};
+
+// Thread 0: tile range of this (r, split) and the first tile index from which the mask
+// is needed (tiles below it are prompt-only and inside every beam's window).
+__device__ __forceinline__ void item_setup(const AttnParams& p, int r, int split, ItemInfo* info) {
+  const size_t mbase = (size_t)r * p.cap;
+  const int N = p.nn[r], t = p.tlen[r];
+  int lo = 0, lo_dep_max = INT_MIN;
+  if (p.window > 0) {
+    int lo_dep = INT_MAX;
+    for (int j = 0; j < p.b_live; ++j) {
+      const int d = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + j]] - p.window + 1;
+      lo_dep = min(lo_dep, d);
+      lo_dep_max = max(lo_dep_max, d);
+    }
+    int a = 0, b = N;  // first slot with depth >= lo_dep (depth non-decreasing)
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (p.depth[mbase + mid] < lo_dep) a = mid + 1; else b = mid;
+    }
+    lo = a;
+  }
+  const int first = lo / TC_TR;
+  const int total = (N + TC_TR - 1) / TC_TR - first;
+  const int per = (total + p.splits - 1) / p.splits;
+  const int tb = min(total, split * per), te = min(total, (split + 1) * per);
+  info->tile0 = first + tb;
+  info->ntiles = te - tb;
+  info->lo = lo;
+  info->N = N;
+  info->t = t;
+  // unmasked tiles: every row n satisfies n < t (prompt: depth = n), n < N and
+  // depth = n >= every beam's lower depth  <=>  tile in [ceil(lo_dep_max / TR), t / TR)
+  const int fmin = p.window > 0 ? (max(lo_dep_max, 0) + TC_TR - 1) / TC_TR : 0;
+  info->fast_from = fmin;  // fast tiles: fmin <= tile < min(t, N) / TR
+}
+
+template <int D, int STAGES>
+__device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUtensorMap* vmap,
+                                              const AttnParams& p, int r, int h,
+                                              const ItemInfo& it, uint8_t* ring, uint64_t* full,
+                                              uint64_t* empty) {
+  using RG = Ring<D, STAGES>;
+  const int row_base = (r * p.Hkv + h) * p.cap;
+  const size_t mbase = (size_t)r * p.cap;
+  for (int i = 0; i < it.ntiles; ++i) {
+    const int s = i % STAGES;
+    const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+    mbar_wait(&empty[s], ph ^ 1u);
+    const uint32_t st = smem_u32(ring + s * RG::STAGE_BYTES);
+    const int n0 = (it.tile0 + i) * TC_TR;
+    // mask / depth words clamped to the [R][cap] arrays (cap % 4 == 0: 16-byte granules)
+    const uint32_t mdb = (uint32_t)min(TC_TR, p.cap - n0) * 4u;
+    mbar_expect_tx(&full[s], 2 * RG::TILE_BYTES + 2 * mdb);
+#pragma unroll
+    for (int bx = 0; bx < D / TC_CW; ++bx) {
+      tma_load_2d(st + bx * TC_TR * 64, kmap, bx * TC_CW, row_base + n0, &full[s]);
+      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vmap, bx * TC_CW, row_base + n0, &full[s]);
+    }
+    bulk_load_1d(st + 2 * RG::TILE_BYTES, p.mask + mbase + n0, mdb, &full[s]);
+    bulk_load_1d(st + 2 * RG::TILE_BYTES + TC_TR * 4, p.depth + mbase + n0, mdb, &full[s]);
+  }
+}
+
+// =========================================================================================
+// narrow: Qg <= 8 * NQ (NQ in {1, 2}); CTA = producer warp + one consumer warp
+// =========================================================================================
+template <int D, int NQ, int ST>
+struct NarrowCfg {
+  static constexpr int STAGES = ST;
+  using RG = Ring<D, STAGES>;
+  static constexpr int KS = D / 16;     // k-steps of S^T (over D)
+  static constexpr int DM = D / 16;     // m-tiles of O^T (over D)
+  // epilogue staging [8*NQ][D+4] floats aliases the ring (all tiles consumed by then)
+  static_assert(NQ * 8 * (D + 4) * 4 <= RG::RING_BYTES, "staging must fit in the ring");
+  static constexpr int SMEM = RG::RING_BYTES + 2 * STAGES * 8 + 64 + 1024;
+};
+
+template <int D, int NQ, int ST>
+__global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUtensorMap kmap,
+                                                    const __grid_constant__ CUtensorMap vmap,
+                                                    const AttnParams p) {
+  using C = NarrowCfg<D, NQ, ST>;
+  using RG = typename C::RG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ring = smem;
+  float* stage_out = (float*)smem;  // epilogue only
+  uint64_t* full = (uint64_t*)(smem + RG::RING_BYTES);
   uint64_t* empty = full + C::STAGES;
-  int* s_info = (int*)(empty + C::STAGES);  // [0] tile0, [1] ntiles, [2] lo slot
+  ItemInfo* info = (ItemInfo*)(empty + C::STAGES);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
-  const size_t mbase = (size_t)r * p.cap;
-  const int N = p.nn[r], t = p.tlen[r];
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::NC);
+      mbar_init(&empty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // window: slot lower bound from the smallest per-beam lower depth (depth monotone)
-    int lo = 0;
-    if (p.window > 0) {
-      int lo_dep = INT_MAX;
-      for (int j = 0; j < p.b_live; ++j)
-        lo_dep = min(lo_dep, p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + j]] - p.window + 1);
-      int a = 0, b = N;
-      while (a < b) {
-        const int mid = (a + b) >> 1;
-        if (p.depth[mbase + mid] < lo_dep) a = mid + 1; else b = mid;
-      }
-      lo = a;
-    }
-    const int first = lo / TC_TR;
-    const int total = (N + TC_TR - 1) / TC_TR - first;
-    const int per = (total + p.splits - 1) / p.splits;
-    const int tb = min(total, split * per), te = min(total, (split + 1) * per);
-    s_info[0] = first + tb;
-    s_info[1] = te - tb;
-    s_info[2] = lo;
+    item_setup(p, r, split, info);
   }
   __syncthreads();
-  const int tile0 = s_info[0], ntiles = s_info[1];
-
+  const ItemInfo it = *info;
   if (warp == 0) {
-    // ===== producer =====
-    if (lane == 0) {
-      const int row_base = (r * p.Hkv + h) * p.cap;
-      for (int i = 0; i < ntiles; ++i) {
-        const int s = i % C::STAGES;
-        const uint32_t ph = (uint32_t)(i / C::STAGES) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        uint8_t* st = smem + s * C::STAGE_BYTES;
-        const int n0 = (tile0 + i) * TC_TR;
-        // mask / depth words of the tile, clamped to the [R][cap] arrays (cap % 4 == 0 =>
-        // 16-byte aligned, 16-byte multiple)
-        const uint32_t mdb = (uint32_t)min(TC_TR, p.cap - n0) * 4u;
-        mbar_expect_tx(&full[s], 2 * C::TILE_BYTES + 2 * mdb);
-#pragma unroll
-        for (int bx = 0; bx < D / TC_CW; ++bx) {
-          tma_load_2d(st + bx * TC_TR * 64, &kmap, bx * TC_CW, row_base + n0, &full[s]);
-          tma_load_2d(st + C::TILE_BYTES + bx * TC_TR * 64, &vmap, bx * TC_CW, row_base + n0,
-                      &full[s]);
-        }
-        bulk_load_1d(st + 2 * C::TILE_BYTES, p.mask + mbase + n0, mdb, &full[s]);
-        bulk_load_1d(st + 2 * C::TILE_BYTES + TC_TR * 4, p.depth + mbase + n0, mdb, &full[s]);
-      }
-    }
+    if (lane == 0) producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
     return;
   }
+  // ===== consumer warp =====
+  const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
+  const int gq = lane >> 2, cq = lane & 3;
+  const size_t mbase = (size_t)r * p.cap;
+  // queries held by this thread in the S^T / O^T fragments: columns 2cq, 2cq+1 of each n-tile
+  int beam[NQ][2], lod[NQ][2];
+  bool qok[NQ][2];
+#pragma unroll
+  for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int m = nq * 8 + cq * 2 + e;
+      qok[nq][e] = m < Qg;
+      beam[nq][e] = m < Qg ? m / g : 0;
+      lod[nq][e] = INT_MIN;
+      if (p.window > 0 && m < Qg)
+        lod[nq][e] = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam[nq][e]]] - p.window + 1;
+    }
+  // Q as the B operand (B[k = d][n = query]): b0 = Q[query gq][ks*16 + 2cq..], b1 = +8
+  uint32_t qb[NQ][C::KS][2];
+  {
+    const __nv_bfloat16* q = (const __nv_bfloat16*)p.q;
+#pragma unroll
+    for (int nq = 0; nq < NQ; ++nq) {
+      const int m = nq * 8 + gq;
+      const __nv_bfloat16* src = nullptr;
+      if (m < Qg) src = q + (((size_t)r * p.b_live + m / g) * p.Hq + h * g + m % g) * D;
+#pragma unroll
+      for (int ks = 0; ks < C::KS; ++ks) {
+        qb[nq][ks][0] = src ? *(const uint32_t*)(src + ks * 16 + cq * 2) : 0u;
+        qb[nq][ks][1] = src ? *(const uint32_t*)(src + ks * 16 + 8 + cq * 2) : 0u;
+      }
+    }
+  }
+  float o[C::DM][NQ][4];
+#pragma unroll
+  for (int dm = 0; dm < C::DM; ++dm)
+#pragma unroll
+    for (int nq = 0; nq < NQ; ++nq) o[dm][nq][0] = o[dm][nq][1] = o[dm][nq][2] = o[dm][nq][3] = 0.f;
+  float mq[NQ][2], lq[NQ][2];
+#pragma unroll
+  for (int nq = 0; nq < NQ; ++nq) mq[nq][0] = mq[nq][1] = -INFINITY, lq[nq][0] = lq[nq][1] = 0.f;
+  const float sc = p.scale_log2;
+  const int fast_end = min(it.t, it.N) / TC_TR;
 
-  // ===== consumers =====
-  const int cw = warp - 1;
-  const int mt = cw % MT, rs = cw / MT;
-  const int gq = lane >> 2, cq = lane & 3;  // fragment row group / column quad
-  // this thread's two query rows (g, g+8) -> beam index and window lower depth
+  for (int i = 0; i < it.ntiles; ++i) {
+    const int s = i % C::STAGES;
+    mbar_wait(&full[s], (uint32_t)(i / C::STAGES) & 1u);
+    const uint8_t* st = ring + s * RG::STAGE_BYTES;
+    const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + RG::TILE_BYTES);
+    const int tile = it.tile0 + i;
+    const int n0 = tile * TC_TR;
+    const bool fast = tile >= it.fast_from && tile < fast_end;
+    // ---- S^T = K Q^T : 4 row groups of 16 ----
+    float sacc[4][NQ][4];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+#pragma unroll
+      for (int nq = 0; nq < NQ; ++nq) sacc[mt][nq][0] = sacc[mt][nq][1] = sacc[mt][nq][2] = sacc[mt][nq][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < C::KS; ++ks) {
+        const int row = mt * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int col = ks * 16 + (lane >> 4) * 8;
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(kbase + tile_off(row, col), a0, a1, a2, a3);
+#pragma unroll
+        for (int nq = 0; nq < NQ; ++nq) mma_bf16(sacc[mt][nq], a0, a1, a2, a3, qb[nq][ks][0], qb[nq][ks][1]);
+      }
+    }
+    // ---- scale, mask, running max per query column ----
+    float tmax[NQ][2];
+#pragma unroll
+    for (int nq = 0; nq < NQ; ++nq) tmax[nq][0] = tmax[nq][1] = -INFINITY;
+    if (fast) {
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float v = qok[nq][e & 1] ? sacc[mt][nq][e] * sc : -INFINITY;
+            sacc[mt][nq][e] = v;
+            tmax[nq][e & 1] = fmaxf(tmax[nq][e & 1], v);
+          }
+    } else {
+      const uint32_t* tmask = (const uint32_t*)(st + 2 * RG::TILE_BYTES);
+      const int* tdep = (const int*)(st + 2 * RG::TILE_BYTES + TC_TR * 4);
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // fragment rows gq (hh=0) and gq+8 (hh=1)
+          const int lr = mt * 16 + gq + hh * 8;
+          const int n = n0 + lr;
+          const bool rowin = n < it.N;
+          const uint32_t mw = rowin ? tmask[lr] : 0u;
+          const int dep = rowin ? tdep[lr] : INT_MIN;
+          const bool prompt = n < it.t;
+#pragma unroll
+          for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const bool ok = rowin && qok[nq][e] && (prompt || ((mw >> beam[nq][e]) & 1u)) &&
+                              dep >= lod[nq][e];
+              const float v = ok ? sacc[mt][nq][hh * 2 + e] * sc : -INFINITY;
+              sacc[mt][nq][hh * 2 + e] = v;
+              tmax[nq][e] = fmaxf(tmax[nq][e], v);
+            }
+        }
+    }
+    float alpha[NQ][2];
+#pragma unroll
+    for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        float v = tmax[nq][e];
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
+        const float mnew = fmaxf(mq[nq][e], v);
+        alpha[nq][e] = (mnew == -INFINITY) ? 1.f : exp2f(mq[nq][e] - mnew);
+        mq[nq][e] = mnew;
+        lq[nq][e] *= alpha[nq][e];
+      }
+    // ---- P^T -> B fragments of O^T = V^T P^T (movmatrix.trans) ----
+    uint32_t pb[4][NQ][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nq = 0; nq < NQ; ++nq) {
+        float pv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float x = sacc[mt][nq][e];
+          pv[e] = (x == -INFINITY) ? 0.f : exp2f(x - mq[nq][e & 1]);
+          lq[nq][e & 1] += pv[e];
+        }
+        pb[mt][nq][0] = movm_t(pack_bf16(pv[0], pv[1]));  // rows gq      -> B rows 0..7
+        pb[mt][nq][1] = movm_t(pack_bf16(pv[2], pv[3]));  // rows gq + 8  -> B rows 8..15
+      }
+#pragma unroll
+    for (int dm = 0; dm < C::DM; ++dm)
+#pragma unroll
+      for (int nq = 0; nq < NQ; ++nq) {
+        o[dm][nq][0] *= alpha[nq][0];
+        o[dm][nq][1] *= alpha[nq][1];
+        o[dm][nq][2] *= alpha[nq][0];
+        o[dm][nq][3] *= alpha[nq][1];
+      }
+    // ---- O^T += V^T P^T : A = V^T via ldmatrix.trans (16 d x 16 rows) ----
+#pragma unroll
+    for (int dm = 0; dm < C::DM; ++dm)
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        const int mi = lane >> 3;
+        const int row = kc * 16 + (lane & 7) + (mi >> 1) * 8;
+        const int col = dm * 16 + (mi & 1) * 8;
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(vbase + tile_off(row, col), a0, a1, a2, a3);
+#pragma unroll
+        for (int nq = 0; nq < NQ; ++nq) mma_bf16(o[dm][nq], a0, a1, a2, a3, pb[kc][nq][0], pb[kc][nq][1]);
+      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  // ---- epilogue: column sums over the 8 lanes of a column quad, transpose via smem ----
+#pragma unroll
+  for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      float v = lq[nq][e];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      lq[nq][e] = v;
+    }
+  constexpr int RW = D + 4;
+#pragma unroll
+  for (int dm = 0; dm < C::DM; ++dm)
+#pragma unroll
+    for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int d = dm * 16 + gq + (e >> 1) * 8;
+        const int m = nq * 8 + cq * 2 + (e & 1);
+        stage_out[m * RW + d] = o[dm][nq][e];
+      }
+  if (gq == 0) {
+#pragma unroll
+    for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = nq * 8 + cq * 2 + e;
+        stage_out[m * RW + D] = mq[nq][e];
+        stage_out[m * RW + D + 1] = lq[nq][e];
+      }
+  }
+  __syncwarp();
+  const int nqr = min(Qg, NQ * 8);
+  for (int m = 0; m < nqr; ++m) {
+    const float M = stage_out[m * RW + D], Ls = stage_out[m * RW + D + 1];
+    const int j = m / g, ii = m % g;
+    if (p.splits == 1) {
+      __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
+      const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
+      for (int d = lane * 2; d < D; d += 64)
+        *(uint32_t*)(op + d) = pack_bf16(stage_out[m * RW + d] * inv, stage_out[m * RW + d + 1] * inv);
+      if (lane == 0) {
+        if (Ls == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
+        if (p.lse)
+          p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
+              Ls > 0.f ? (M + log2f(Ls)) * 0.69314718055994531f : -INFINITY;
+      }
+    } else {
+      float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + m) * (D + 2);
+      for (int d = lane; d < D; d += 32) pp[d] = stage_out[m * RW + d];
+      if (lane == 0) {
+        pp[D] = M;
+        pp[D + 1] = Ls;
+      }
+    }
+  }
+}
+
+// =========================================================================================
+// wide: 16 < Qg <= 16 * MT; CTA = producer warp + MT consumer warps (one query m-tile each)
+// =========================================================================================
+template <int D, int MT>
+struct WideCfg {
+  static constexpr int STAGES = D >= 128 ? 3 : 4;
+  using RG = Ring<D, STAGES>;
+  static constexpr int KS = D / 16;
+  static constexpr int DT = D / 8;
+  static constexpr int NT = TC_TR / 8;  // S n-tiles per tile
+  static constexpr int SMEM = RG::RING_BYTES + 2 * STAGES * 8 + 64 + 1024;
+  static constexpr int THREADS = 32 * (MT + 1);
+};
+
+template <int D, int MT>
+__global__ void __launch_bounds__(WideCfg<D, MT>::THREADS) k_attn_wide(
+    const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+    const AttnParams p) {
+  using C = WideCfg<D, MT>;
+  using RG = typename C::RG;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ring = smem;
+  uint64_t* full = (uint64_t*)(smem + RG::RING_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  ItemInfo* info = (ItemInfo*)(empty + C::STAGES);
+
+  const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    item_setup(p, r, split, info);
+  }
+  __syncthreads();
+  const ItemInfo it = *info;
+  if (warp == 0) {
+    if (lane == 0) producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+    return;
+  }
+  const int mt = warp - 1;
+  const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
+  const int gq = lane >> 2, cq = lane & 3;
+  const size_t mbase = (size_t)r * p.cap;
   int qm[2], beam[2], lod[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
@@ -207,185 +517,161 @@ __global__ void __launch_bounds__(TcCfg<D, MT>::THREADS) k_attn_tc(
   {
     const __nv_bfloat16* qb = (const __nv_bfloat16*)p.q;
 #pragma unroll
-    for (int ks = 0; ks < C::KS; ++ks) {
+    for (int ks = 0; ks < C::KS; ++ks)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int row = (u & 1) ? qm[1] : qm[0];
         const int col = ks * 16 + (u >> 1) * 8 + cq * 2;
         uint32_t v = 0u;
-        if (row < Qg) {
-          const int j = row / g, i = row % g;
-          const __nv_bfloat16* src = qb + (((size_t)r * p.b_live + j) * p.Hq + h * g + i) * D + col;
-          v = *(const uint32_t*)src;
-        }
+        if (row < Qg)
+          v = *(const uint32_t*)(qb + (((size_t)r * p.b_live + row / g) * p.Hq + h * g + row % g) * D + col);
         qa[ks][u] = v;
       }
-    }
   }
   float o[C::DT][4];
 #pragma unroll
   for (int i = 0; i < C::DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   const float sc = p.scale_log2;
+  const int fast_end = min(it.t, it.N) / TC_TR;
+  const bool active = mt * 16 < Qg;  // (MT is the smallest that covers Qg: always true)
 
-  for (int i = 0; i < ntiles; ++i) {
+  for (int i = 0; i < it.ntiles; ++i) {
     const int s = i % C::STAGES;
-    const uint32_t ph = (uint32_t)(i / C::STAGES) & 1u;
-    mbar_wait(&full[s], ph);
-    const uint8_t* st = smem + s * C::STAGE_BYTES;
-    const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + C::TILE_BYTES);
-    const uint32_t* tmask = (const uint32_t*)(st + 2 * C::TILE_BYTES);
-    const int* tdep = (const int*)(st + 2 * C::TILE_BYTES + TC_TR * 4);
-    const int n0 = (tile0 + i) * TC_TR;
-    const int r0 = rs * C::RSZ;  // first row of this warp's slice within the tile
-    // ---- S = Q K^T over the slice ----
-    float sacc[C::NT][4];
+    mbar_wait(&full[s], (uint32_t)(i / C::STAGES) & 1u);
+    const uint8_t* st = ring + s * RG::STAGE_BYTES;
+    const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + RG::TILE_BYTES);
+    const int tile = it.tile0 + i;
+    const int n0 = tile * TC_TR;
+    const bool fast = tile >= it.fast_from && tile < fast_end;
+    if (active) {
+      float sacc[C::NT][4];
 #pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+      for (int nt = 0; nt < C::NT; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
 #pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt) {
+      for (int ks = 0; ks < C::KS; ks += 2)
 #pragma unroll
-      for (int ks = 0; ks < C::KS; ks += 2) {
-        // x4: matrices (rows nt*8.., k ks*16+0..7), (.., +8..15), (.., (ks+1)*16+0..7), (+8..15)
-        const int row = r0 + nt * 8 + (lane & 7);
-        const int col = ks * 16 + (lane >> 3) * 8;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kbase + tile_off(row, col), b0, b1, b2, b3);
-        mma_bf16(sacc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-        if (ks + 1 < C::KS) mma_bf16(sacc[nt], qa[ks + 1][0], qa[ks + 1][1], qa[ks + 1][2], qa[ks + 1][3], b2, b3);
+        for (int nt = 0; nt < C::NT; ++nt) {
+          const int row = nt * 8 + (lane & 7);
+          const int col = ks * 16 + (lane >> 3) * 8;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kbase + tile_off(row, col), b0, b1, b2, b3);
+          mma_bf16(sacc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+          mma_bf16(sacc[nt], qa[ks + 1][0], qa[ks + 1][1], qa[ks + 1][2], qa[ks + 1][3], b2, b3);
+        }
+      float tmax[2] = {-INFINITY, -INFINITY};
+      if (fast) {
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int u = e >> 1;
+            const float v = qm[u] < Qg ? sacc[nt][e] * sc : -INFINITY;
+            sacc[nt][e] = v;
+            tmax[u] = fmaxf(tmax[u], v);
+          }
+      } else {
+        const uint32_t* tmask = (const uint32_t*)(st + 2 * RG::TILE_BYTES);
+        const int* tdep = (const int*)(st + 2 * RG::TILE_BYTES + TC_TR * 4);
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int lr = nt * 8 + cq * 2 + cc;
+            const int n = n0 + lr;
+            const bool rowin = n < it.N;
+            const uint32_t mw = rowin ? tmask[lr] : 0u;
+            const int dep = rowin ? tdep[lr] : INT_MIN;
+            const bool prompt = n < it.t;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const bool ok = rowin && qm[u] < Qg && (prompt || ((mw >> beam[u]) & 1u)) && dep >= lod[u];
+              const float v = ok ? sacc[nt][u * 2 + cc] * sc : -INFINITY;
+              sacc[nt][u * 2 + cc] = v;
+              tmax[u] = fmaxf(tmax[u], v);
+            }
+          }
       }
-    }
-    // ---- mask + online softmax (log2 domain) ----
-    float tmax[2] = {-INFINITY, -INFINITY};
+      float alpha[2];
 #pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int u = e >> 1;
-        const int lr = r0 + nt * 8 + cq * 2 + (e & 1);  // row within tile
-        const int n = n0 + lr;
-        const uint32_t mw = tmask[lr];
-        const int dep = tdep[lr];
-        const bool ok = n < N && (n < t || ((mw >> beam[u]) & 1u)) && dep >= lod[u] &&
-                        qm[u] < Qg;  // (n < N also guards stale words past cap)
-        const float v = ok ? sacc[nt][e] * sc : -INFINITY;
-        sacc[nt][e] = v;
-        tmax[u] = fmaxf(tmax[u], v);
+      for (int u = 0; u < 2; ++u) {
+        tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 1));
+        tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 2));
+        const float mnew = fmaxf(mrow[u], tmax[u]);
+        alpha[u] = (mnew == -INFINITY) ? 1.f : exp2f(mrow[u] - mnew);
+        mrow[u] = mnew;
+        lrow[u] *= alpha[u];
       }
-    }
-    float alpha[2];
+      uint32_t pa[C::NT][2];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 1));
-      tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 2));
-      const float mnew = fmaxf(mrow[u], tmax[u]);
-      alpha[u] = (mnew == -INFINITY) ? 1.f : exp2f(mrow[u] - mnew);
-      mrow[u] = mnew;
-    }
-    float psum[2] = {0.f, 0.f};
-    uint32_t pa[C::NT][2];
+      for (int nt = 0; nt < C::NT; ++nt) {
+        float pv[4];
 #pragma unroll
-    for (int nt = 0; nt < C::NT; ++nt) {
-      float pv[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int u = e >> 1;
-        pv[e] = (sacc[nt][e] == -INFINITY) ? 0.f : exp2f(sacc[nt][e] - mrow[u]);
-        psum[u] += pv[e];
+        for (int e = 0; e < 4; ++e) {
+          const int u = e >> 1;
+          pv[e] = (sacc[nt][e] == -INFINITY) ? 0.f : exp2f(sacc[nt][e] - mrow[u]);
+          lrow[u] += pv[e];
+        }
+        pa[nt][0] = pack_bf16(pv[0], pv[1]);
+        pa[nt][1] = pack_bf16(pv[2], pv[3]);
       }
-      pa[nt][0] = pack_bf16(pv[0], pv[1]);
-      pa[nt][1] = pack_bf16(pv[2], pv[3]);
-    }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) lrow[u] = lrow[u] * alpha[u] + psum[u];
+      for (int dt = 0; dt < C::DT; ++dt) {
+        o[dt][0] *= alpha[0];
+        o[dt][1] *= alpha[0];
+        o[dt][2] *= alpha[1];
+        o[dt][3] *= alpha[1];
+      }
 #pragma unroll
-    for (int dt = 0; dt < C::DT; ++dt) {
-      o[dt][0] *= alpha[0];
-      o[dt][1] *= alpha[0];
-      o[dt][2] *= alpha[1];
-      o[dt][3] *= alpha[1];
-    }
-    // ---- O += P V : k = slice rows (16 per mma), n = D ----
+      for (int kc = 0; kc < C::NT / 2; ++kc) {
+        const uint32_t a0 = pa[2 * kc][0], a1 = pa[2 * kc][1], a2 = pa[2 * kc + 1][0],
+                       a3 = pa[2 * kc + 1][1];
 #pragma unroll
-    for (int kc = 0; kc < C::NT / 2; ++kc) {
-      const uint32_t a0 = pa[2 * kc][0], a1 = pa[2 * kc][1], a2 = pa[2 * kc + 1][0],
-                     a3 = pa[2 * kc + 1][1];
-#pragma unroll
-      for (int dt = 0; dt < C::DT; dt += 2) {
-        // x4.trans: (rows k0..7, d dt*8..), (rows k8..15, d dt*8..), (k0..7, (dt+1)*8..), (k8..15, ..)
-        const int row = r0 + kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        const int col = dt * 8 + (lane >> 4) * 8;
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vbase + tile_off(row, col), b0, b1, b2, b3);
-        mma_bf16(o[dt], a0, a1, a2, a3, b0, b1);
-        mma_bf16(o[dt + 1], a0, a1, a2, a3, b2, b3);
+        for (int dt = 0; dt < C::DT; dt += 2) {
+          const int row = kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+          const int col = dt * 8 + (lane >> 4) * 8;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vbase + tile_off(row, col), b0, b1, b2, b3);
+          mma_bf16(o[dt], a0, a1, a2, a3, b0, b1);
+          mma_bf16(o[dt + 1], a0, a1, a2, a3, b2, b3);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  // quad-reduce the row sums (each thread holds partial sums of its columns)
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     lrow[u] += __shfl_xor_sync(0xffffffffu, lrow[u], 1);
     lrow[u] += __shfl_xor_sync(0xffffffffu, lrow[u], 2);
   }
-
-  // ---- merge the RS row-slice warps of each m-tile through shared memory ----
-  // all consumers must be done with the ring before it is reused
-  asm volatile("bar.sync 1, %0;" ::"r"(C::NC * 32));
-  float* red = (float*)smem;  // [NC][16][D + 2]
-  const int RW = D + 2;
-  float* mine = red + (size_t)cw * 16 * RW;
 #pragma unroll
-  for (int dt = 0; dt < C::DT; ++dt) {
-    const int col = dt * 8 + cq * 2;
-    mine[gq * RW + col] = o[dt][0];
-    mine[gq * RW + col + 1] = o[dt][1];
-    mine[(gq + 8) * RW + col] = o[dt][2];
-    mine[(gq + 8) * RW + col + 1] = o[dt][3];
-  }
-  if (cq == 0) {
-    mine[gq * RW + D] = mrow[0];
-    mine[gq * RW + D + 1] = lrow[0];
-    mine[(gq + 8) * RW + D] = mrow[1];
-    mine[(gq + 8) * RW + D + 1] = lrow[1];
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(C::NC * 32));
-  // thread -> (query row within m-tile, column range); warps of slice 0 finalize
-  if (rs == 0) {
-    for (int e = lane; e < 16 * D; e += 32) {
-      const int qr = e / D, d = e % D;
-      const int m = mt * 16 + qr;
-      if (m >= Qg) continue;
-      float M = -INFINITY;
+  for (int u = 0; u < 2; ++u) {
+    const int m = qm[u];
+    if (m >= Qg) continue;
+    const int j = m / g, ii = m % g;
+    if (p.splits == 1) {
+      __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
+      const float inv = lrow[u] > 0.f ? 1.f / lrow[u] : 0.f;
 #pragma unroll
-      for (int x = 0; x < C::RS; ++x) M = fmaxf(M, red[((size_t)(x * MT + mt) * 16 + qr) * RW + D]);
-      float Lsum = 0.f, acc = 0.f;
-#pragma unroll
-      for (int x = 0; x < C::RS; ++x) {
-        const float* src = red + ((size_t)(x * MT + mt) * 16 + qr) * RW;
-        const float w = src[D] == -INFINITY ? 0.f : exp2f(src[D] - M);
-        Lsum += src[D + 1] * w;
-        acc += src[d] * w;
+      for (int dt = 0; dt < C::DT; ++dt)
+        *(uint32_t*)(op + dt * 8 + cq * 2) = pack_bf16(o[dt][u * 2] * inv, o[dt][u * 2 + 1] * inv);
+      if (cq == 0) {
+        if (lrow[u] == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
+        if (p.lse)
+          p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
+              lrow[u] > 0.f ? (mrow[u] + log2f(lrow[u])) * 0.69314718055994531f : -INFINITY;
       }
-      const int j = m / g, ii = m % g;
-      if (p.splits == 1) {
-        __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
-        op[d] = __float2bfloat16_rn(Lsum > 0.f ? acc / Lsum : 0.f);
-        if (d == 0) {
-          if (Lsum == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
-          if (p.lse)
-            p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
-                Lsum > 0.f ? (M + log2f(Lsum)) * 0.69314718055994531f : -INFINITY;
-        }
-      } else {
-        float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + m) * (D + 2);
-        pp[d] = acc;
-        if (d == 0) {
-          pp[D] = M;
-          pp[D + 1] = Lsum;
-        }
+    } else {
+      float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + m) * (D + 2);
+#pragma unroll
+      for (int dt = 0; dt < C::DT; ++dt) {
+        pp[dt * 8 + cq * 2] = o[dt][u * 2];
+        pp[dt * 8 + cq * 2 + 1] = o[dt][u * 2 + 1];
+      }
+      if (cq == 0) {
+        pp[D] = mrow[u];
+        pp[D + 1] = lrow[u];
       }
     }
   }
@@ -415,60 +701,116 @@ static int make_map(CUtensorMap* map, const void* base, int D, long rows) {
   CUresult rc = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (rc != CUDA_SUCCESS) return trie_set_error(TRIE_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
+  if (rc != CUDA_SUCCESS)
+    return trie_set_error(TRIE_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
   return TRIE_OK;
 }
 
-template <int D, int MT>
-static int launch_tc_t(const AttnParams& p, cudaStream_t s) {
-  using C = TcCfg<D, MT>;
+// Small direct-mapped cache of encoded tensor maps (the pools of a model are a fixed set
+// of per-layer base pointers), so a decode step does not re-encode 2L descriptors.
+struct MapEntry {
+  const void* base;
+  long rows;
+  int D;
+  CUtensorMap map;
+};
+static int cached_map(CUtensorMap* out, const void* base, int D, long rows) {
+  static MapEntry cache[512];
+  const size_t slot = (((uintptr_t)base >> 8) ^ ((uintptr_t)base >> 20)) % 512;
+  MapEntry& e = cache[slot];
+  if (e.base != base || e.rows != rows || e.D != D) {
+    const int rc = make_map(&e.map, base, D, rows);
+    if (rc) {
+      e.base = nullptr;
+      return rc;
+    }
+    e.base = base;
+    e.rows = rows;
+    e.D = D;
+  }
+  *out = e.map;
+  return TRIE_OK;
+}
+
+template <typename Kern>
+static int launch_with(Kern kern, int smem, int threads, const AttnParams& p, cudaStream_t s,
+                       int D, bool* attr_done) {
   CUtensorMap km, vm;
   const long rows = (long)p.R * p.Hkv * p.cap;
-  int rc = make_map(&km, p.k, D, rows);
-  if (!rc) rc = make_map(&vm, p.v, D, rows);
+  int rc = cached_map(&km, p.k, D, rows);
+  if (!rc) rc = cached_map(&vm, p.v, D, rows);
   if (rc) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_attn_tc<D, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr_set = true;
+  if (!*attr_done) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    *attr_done = true;
   }
   dim3 grid(p.Hkv, p.R, p.splits);
-  k_attn_tc<D, MT><<<grid, C::THREADS, C::SMEM, s>>>(km, vm, p);
+  kern<<<grid, threads, smem, s>>>(km, vm, p);
   rc = trie_check_launch("k_attn_tc");
   if (rc) return rc;
   if (p.splits > 1) rc = launch_attn_combine_bf16(p, s);
   return rc;
 }
 
-template <int D>
-static int launch_tc_d(const AttnParams& p, cudaStream_t s, int MT) {
-  switch (MT) {
-    case 1: return launch_tc_t<D, 1>(p, s);
-    case 2: return launch_tc_t<D, 2>(p, s);
-    case 4: return launch_tc_t<D, 4>(p, s);
-    case 8: return launch_tc_t<D, 8>(p, s);
+template <int D, int NQ, int ST>
+static int launch_narrow_st(const AttnParams& p, cudaStream_t s) {
+  static bool done = false;
+  return launch_with(k_attn_narrow<D, NQ, ST>, NarrowCfg<D, NQ, ST>::SMEM, 64, p, s, D, &done);
+}
+// Stages per narrow CTA (tuning knob TRIE_NARROW_STAGES in {2, 3, 4}).  Default 2: at
+// D = 96 a 2-stage CTA needs ~50 KB, so 3-4 CTAs (3-4 consumer warps, 6-8 tiles in
+// flight) share an SM; measured r01 on the Phi workload: 2 -> 5.81 TB/s, 3 -> 5.18,
+// 4 -> 5.34 (more independent streams beat deeper per-stream rings).
+static int narrow_stages() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TRIE_NARROW_STAGES");
+    v = e ? atoi(e) : 2;
+    if (v < 2 || v > 4) v = 2;
   }
-  return 1;
+  return v;
+}
+template <int D, int NQ>
+static int launch_narrow(const AttnParams& p, cudaStream_t s) {
+  switch (narrow_stages()) {
+    case 2: return launch_narrow_st<D, NQ, 2>(p, s);
+    case 3: return launch_narrow_st<D, NQ, 3>(p, s);
+    case 4: return launch_narrow_st<D, NQ, 4>(p, s);
+    default: return launch_narrow_st<D, NQ, 2>(p, s);
+  }
+}
+template <int D, int MT>
+static int launch_wide(const AttnParams& p, cudaStream_t s) {
+  static bool done = false;
+  return launch_with(k_attn_wide<D, MT>, WideCfg<D, MT>::SMEM, WideCfg<D, MT>::THREADS, p, s, D,
+                     &done);
+}
+
+template <int D>
+static int launch_d(const AttnParams& p, cudaStream_t s) {
+  const int Qg = p.b_live * (p.Hq / p.Hkv);
+  if (Qg <= 8) return launch_narrow<D, 1>(p, s);
+  if (Qg <= 16) return launch_narrow<D, 2>(p, s);
+  if (Qg <= 32) return launch_wide<D, 2>(p, s);
+  if (Qg <= 64) return launch_wide<D, 4>(p, s);
+  return launch_wide<D, 8>(p, s);
 }
 
 bool attn_tc_supported(const AttnParams& p) {
   const int Qg = p.b_live * (p.Hq / p.Hkv);
   if (!p.bf16 || Qg > 128 || p.cap % 4) return false;
   if (p.D != 64 && p.D != 96 && p.D != 128) return false;
-  // 16-byte aligned pools for TMA
-  if (((uintptr_t)p.k | (uintptr_t)p.v) & 15) return false;
+  if (((uintptr_t)p.k | (uintptr_t)p.v) & 15) return false;  // TMA needs 16-B aligned pools
   return true;
 }
 
 int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
-  const int Qg = p.b_live * (p.Hq / p.Hkv);
-  const int MT = Qg <= 16 ? 1 : Qg <= 32 ? 2 : Qg <= 64 ? 4 : 8;
   switch (p.D) {
-    case 64: return launch_tc_d<64>(p, s, MT);
-    case 96: return launch_tc_d<96>(p, s, MT);
-    case 128: return launch_tc_d<128>(p, s, MT);
+    case 64: return launch_d<64>(p, s);
+    case 96: return launch_d<96>(p, s);
+    case 128: return launch_d<128>(p, s);
   }
-  return 1;
+  return trie_set_error(TRIE_EINVAL, "tensor-core attention: unsupported head_dim %d", p.D);
 }
 
 }  // namespace trie
