@@ -180,25 +180,38 @@ __global__ void k_attn_combine(const AttnParams p) {
   const int m = gw % Qg, h = (gw / Qg) % p.Hkv, r = gw / (Qg * p.Hkv);
   const int D = p.D;
   const float* base = p.part + (((size_t)r * p.Hkv + h) * p.splits * Qg) * (D + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < p.splits; ++s) M = fmaxf(M, base[((size_t)s * Qg + m) * (D + 2) + D]);
-  float L = 0.f;
-  for (int s = 0; s < p.splits; ++s) {
+  // lanes own splits (<= 64): (m_s, l_s) loaded in parallel, weights w_s = 2^(m_s - M)
+  float ms[2], ls[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int s = lane + 32 * u;
     const float* pp = base + ((size_t)s * Qg + m) * (D + 2);
-    if (pp[D + 1] > 0.f) L += pp[D + 1] * exp2f(pp[D] - M);
+    ms[u] = s < p.splits ? pp[D] : -INFINITY;
+    ls[u] = s < p.splits ? pp[D + 1] : 0.f;
   }
+  const float M = warp_max(fmaxf(ms[0], ms[1]));
+  float ws[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) ws[u] = ls[u] > 0.f ? exp2f(ms[u] - M) : 0.f;
+  const float L = warp_sum(ls[0] * ws[0] + ls[1] * ws[1]);
   const int j = m / g, ii = m % g;
   T* op = (T*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
   const float inv = L > 0.f ? 1.f / L : 0.f;
   if (L == 0.f && lane == 0) latch(p.status, TRIE_ST_EMPTY_ROW);
-  for (int d = lane; d < D; d += 32) {
-    float a = 0.f;
-    for (int s = 0; s < p.splits; ++s) {
-      const float* pp = base + ((size_t)s * Qg + m) * (D + 2);
-      if (pp[D + 1] > 0.f) a += pp[d] * exp2f(pp[D] - M);
-    }
-    op[d] = from_f<T>(a * inv);
+  float acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0.f;
+  for (int s = 0; s < p.splits; ++s) {
+    const float w = __shfl_sync(0xffffffffu, ws[s >> 5], s & 31);
+    if (w == 0.f) continue;  // uniform
+    const float* pp = base + ((size_t)s * Qg + m) * (D + 2);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (lane + 32 * c < D) acc[c] += w * pp[lane + 32 * c];
   }
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (lane + 32 * c < D) op[lane + 32 * c] = from_f<T>(acc[c] * inv);
   if (p.lse && lane == 0)
     p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
         L > 0.f ? (M + log2f(L)) * 0.69314718055994531f : -INFINITY;

@@ -14,18 +14,25 @@ template <typename T>
 __global__ void k_rope_append(T* q, T* k_new, const T* v_new, T* kpool, T* vpool,
                               const int32_t* depth, const int32_t* leaf, int b_live, int Hq,
                               int Hkv, int D, int cap, double log2_theta) {
+  __shared__ float s_cos[128], s_sin[128];  // D <= 256
   const int rj = blockIdx.x;  // r * b_live + j
   const int r = rj / b_live, j = rj % b_live;
   const int slot = leaf[r * TRIE_MAX_BEAMS + j];
   const int pos = depth[(size_t)r * cap + slot];
   const int half = D / 2;
-  const int pairs = (Hq + Hkv) * half;
-  for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
-    const int hh = p / half, i = p % half;
+  // one fp64 angle per frequency, shared by every head of this (request, beam)
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
     const double inv_freq = exp2(-2.0 * (double)i / (double)D * log2_theta);
     double sn, cs;
     sincos((double)pos * inv_freq, &sn, &cs);
-    const float c = (float)cs, s = (float)sn;
+    s_cos[i] = (float)cs;
+    s_sin[i] = (float)sn;
+  }
+  __syncthreads();
+  const int pairs = (Hq + Hkv) * half;
+  for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
+    const int hh = p / half, i = p % half;
+    const float c = s_cos[i], s = s_sin[i];
     T* e;
     if (hh < Hq) {
       e = q + ((size_t)rj * Hq + hh) * D;
