@@ -272,13 +272,14 @@ def run_gpu(args):
     pending = {}
     end_ev = [torch.cuda.Event() for _ in range(2)]
 
+    attn_step = []  # (step index, k in job) per harvested launch; bytes computed afterwards
+
     def harvest(slot):
         var_p, kj_p, i_p = pending.pop(slot)
-        end_ev[slot].synchronize()
-        Np = n_hist[i_p].cpu().numpy()
+        end_ev[slot].synchronize()  # only step i_p; step i_p + 1 keeps the GPU busy
         for e0, e1 in hp.ev[(var_p, slot)]:
             attn_ms.append(e0.elapsed_time(e1))
-            attn_bytes.append(hp.attn_bytes(kj_p, Np))
+            attn_step.append((i_p, kj_p))
 
     t0.record(stream)
     for i in range(args.steps):
@@ -302,6 +303,8 @@ def run_gpu(args):
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
+    nh_all = n_hist.cpu().numpy()
+    attn_bytes = [hp.attn_bytes(kj, nh_all[i]) for i, kj in attn_step]
     st_bits = hp.st.status()
     assert st_bits == 0, f"device status bits {st_bits:#x}"
     ach = float(np.sum(attn_bytes) / (np.sum(attn_ms) * 1e-3) / 1e9)

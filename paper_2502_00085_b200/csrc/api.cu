@@ -207,21 +207,28 @@ int trie_rope_kv_append(trie_handle* h, void* q, void* k_new, const void* v_new,
 }
 
 // ---- attention ------------------------------------------------------------------------
-static int attn_splits(const trie_cfg* c, int rows_hint) {
-  int rows = rows_hint > 0 ? rows_hint : c->capacity;
-  const int units = c->n_requests * c->n_kv_heads;
+static trie::AttnParams shape_params(const trie_cfg* cfg, int b_live) {
+  trie::AttnParams p{};
+  p.R = cfg->n_requests;
+  p.b_live = b_live;
+  p.Hq = cfg->n_q_heads;
+  p.Hkv = cfg->n_kv_heads;
+  p.D = cfg->head_dim;
+  p.cap = cfg->capacity;
+  p.bf16 = cfg->kv_dtype == TRIE_BF16;
+  p.scale_log2 = 1.4426950408889634f / sqrtf((float)cfg->head_dim);
+  return p;
+}
+
+static int attn_splits(const trie_cfg* c, int b_live, int rows_hint) {
+  const int rows = rows_hint > 0 ? rows_hint : c->capacity;
   static int sm_cache[64] = {0};
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
     if (!sm_cache[dev]) cudaDeviceGetAttribute(&sm_cache[dev], cudaDevAttrMultiProcessorCount, dev);
     if (sm_cache[dev]) sms = sm_cache[dev];
   }
-  const int target = sms * 2;  // two resident CTAs per SM
-  int splits = (target + units - 1) / units;
-  const int max_by_rows = rows / 128 > 0 ? rows / 128 : 1;  // >= 128 rows per split
-  if (splits > max_by_rows) splits = max_by_rows;
-  if (splits > 64) splits = 64;
-  return splits < 1 ? 1 : splits;
+  return trie::attn_plan_splits(shape_params(c, b_live), rows, sms);
 }
 
 static size_t part_bytes(const trie_cfg* c, int b_live, int splits) {
@@ -232,7 +239,7 @@ static size_t part_bytes(const trie_cfg* c, int b_live, int splits) {
 
 size_t trie_attn_scratch_bytes(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint) {
   if (validate(cfg)) return 0;
-  const int splits = attn_splits(cfg, rows_hint);
+  const int splits = attn_splits(cfg, b_live, rows_hint);
   // split partials + a derived beam_mask when the caller passes none
   return align_up(part_bytes(cfg, b_live, splits)) +
          align_up((size_t)cfg->n_requests * cfg->capacity * 4) + 256;
@@ -249,7 +256,7 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
   if (!q || !k_pool || !v_pool || !prompt_len || !depth || !leaf_ids || !n_nodes || !out)
     return trie_set_error(TRIE_EINVAL, "null argument");
   if (window < 0) return trie_set_error(TRIE_EINVAL, "window < 0");
-  const int splits = attn_splits(cfg, rows_hint);
+  const int splits = attn_splits(cfg, b_live, rows_hint);
   const size_t pb = align_up(part_bytes(cfg, b_live, splits));
   const size_t mb = align_up((size_t)cfg->n_requests * cfg->capacity * 4);
   const size_t need = pb + (beam_mask ? 0 : mb);
@@ -263,7 +270,7 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
     if (rc) return rc;
     beam_mask = derived;
   }
-  trie::AttnParams p;
+  trie::AttnParams p = shape_params(cfg, b_live);
   p.q = q;
   p.k = k_pool;
   p.v = v_pool;
@@ -276,16 +283,8 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
   p.mask = beam_mask;
   p.part = (float*)scratch;
   p.status = nullptr;
-  p.R = cfg->n_requests;
-  p.b_live = b_live;
-  p.Hq = cfg->n_q_heads;
-  p.Hkv = cfg->n_kv_heads;
-  p.D = cfg->head_dim;
-  p.cap = cfg->capacity;
   p.window = window;
   p.splits = splits;
-  p.scale_log2 = 1.4426950408889634f / sqrtf((float)cfg->head_dim);
-  p.bf16 = cfg->kv_dtype == TRIE_BF16;
   if (trie::attn_tc_supported(p)) return trie::launch_attn_tc(p, stream);
   return trie::launch_attn_v1(p, stream);
 }

@@ -26,5 +26,6 @@ int launch_attn_v1(const AttnParams& p, cudaStream_t s);
 int launch_attn_tc(const AttnParams& p, cudaStream_t s);
 bool attn_tc_supported(const AttnParams& p);
 int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s);
+int attn_plan_splits(const AttnParams& p, int rows_est, int sms);
 
 }  // namespace trie

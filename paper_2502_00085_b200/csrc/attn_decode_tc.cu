@@ -732,31 +732,32 @@ static int cached_map(CUtensorMap* out, const void* base, int D, long rows) {
   return TRIE_OK;
 }
 
+// ---- kernel table: attributes (max dynamic smem, max-shared carveout) set once, the
+// occupancy queried once; the split plan uses it so a launch fills whole waves.
+struct TcKernel {
+  const void* fn;
+  int smem, threads, occ;
+};
+
 template <typename Kern>
-static int launch_with(Kern kern, int smem, int threads, const AttnParams& p, cudaStream_t s,
-                       int D, bool* attr_done) {
-  CUtensorMap km, vm;
-  const long rows = (long)p.R * p.Hkv * p.cap;
-  int rc = cached_map(&km, p.k, D, rows);
-  if (!rc) rc = cached_map(&vm, p.v, D, rows);
-  if (rc) return rc;
-  if (!*attr_done) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    *attr_done = true;
-  }
-  dim3 grid(p.Hkv, p.R, p.splits);
-  kern<<<grid, threads, smem, s>>>(km, vm, p);
-  rc = trie_check_launch("k_attn_tc");
-  if (rc) return rc;
-  if (p.splits > 1) rc = launch_attn_combine_bf16(p, s);
-  return rc;
+static TcKernel make_tc(Kern kern, int smem, int threads) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+  return TcKernel{(const void*)kern, smem, threads, occ > 0 ? occ : 1};
+}
+template <int D, int NQ, int ST>
+static const TcKernel& narrow_k() {
+  static const TcKernel k = make_tc(k_attn_narrow<D, NQ, ST>, NarrowCfg<D, NQ, ST>::SMEM, 64);
+  return k;
+}
+template <int D, int MT>
+static const TcKernel& wide_k() {
+  static const TcKernel k = make_tc(k_attn_wide<D, MT>, WideCfg<D, MT>::SMEM, WideCfg<D, MT>::THREADS);
+  return k;
 }
 
-template <int D, int NQ, int ST>
-static int launch_narrow_st(const AttnParams& p, cudaStream_t s) {
-  static bool done = false;
-  return launch_with(k_attn_narrow<D, NQ, ST>, NarrowCfg<D, NQ, ST>::SMEM, 64, p, s, D, &done);
-}
 // Stages per narrow CTA (tuning knob TRIE_NARROW_STAGES in {2, 3, 4}).  Default 2: at
 // D = 96 a 2-stage CTA needs ~50 KB, so 3-4 CTAs (3-4 consumer warps, 6-8 tiles in
 // flight) share an SM; measured r01 on the Phi workload: 2 -> 5.81 TB/s, 3 -> 5.18,
@@ -771,46 +772,75 @@ static int narrow_stages() {
   return v;
 }
 template <int D, int NQ>
-static int launch_narrow(const AttnParams& p, cudaStream_t s) {
+static const TcKernel& narrow_sel() {
   switch (narrow_stages()) {
-    case 2: return launch_narrow_st<D, NQ, 2>(p, s);
-    case 3: return launch_narrow_st<D, NQ, 3>(p, s);
-    case 4: return launch_narrow_st<D, NQ, 4>(p, s);
-    default: return launch_narrow_st<D, NQ, 2>(p, s);
+    case 3: return narrow_k<D, NQ, 3>();
+    case 4: return narrow_k<D, NQ, 4>();
+    default: return narrow_k<D, NQ, 2>();
   }
 }
-template <int D, int MT>
-static int launch_wide(const AttnParams& p, cudaStream_t s) {
-  static bool done = false;
-  return launch_with(k_attn_wide<D, MT>, WideCfg<D, MT>::SMEM, WideCfg<D, MT>::THREADS, p, s, D,
-                     &done);
+template <int D>
+static const TcKernel& select_d(int Qg) {
+  if (Qg <= 8) return narrow_sel<D, 1>();
+  if (Qg <= 16) return narrow_sel<D, 2>();
+  if (Qg <= 32) return wide_k<D, 2>();
+  if (Qg <= 64) return wide_k<D, 4>();
+  return wide_k<D, 8>();
+}
+static const TcKernel* select_tc(int D, int Qg) {
+  switch (D) {
+    case 64: return &select_d<64>(Qg);
+    case 96: return &select_d<96>(Qg);
+    case 128: return &select_d<128>(Qg);
+  }
+  return nullptr;
 }
 
-template <int D>
-static int launch_d(const AttnParams& p, cudaStream_t s) {
+static bool tc_shape_ok(const AttnParams& p) {
   const int Qg = p.b_live * (p.Hq / p.Hkv);
-  if (Qg <= 8) return launch_narrow<D, 1>(p, s);
-  if (Qg <= 16) return launch_narrow<D, 2>(p, s);
-  if (Qg <= 32) return launch_wide<D, 2>(p, s);
-  if (Qg <= 64) return launch_wide<D, 4>(p, s);
-  return launch_wide<D, 8>(p, s);
+  return p.bf16 && Qg <= 128 && p.cap % 4 == 0 && (p.D == 64 || p.D == 96 || p.D == 128);
 }
 
 bool attn_tc_supported(const AttnParams& p) {
-  const int Qg = p.b_live * (p.Hq / p.Hkv);
-  if (!p.bf16 || Qg > 128 || p.cap % 4) return false;
-  if (p.D != 64 && p.D != 96 && p.D != 128) return false;
-  if (((uintptr_t)p.k | (uintptr_t)p.v) & 15) return false;  // TMA needs 16-B aligned pools
-  return true;
+  if (!tc_shape_ok(p)) return false;
+  return ((((uintptr_t)p.k | (uintptr_t)p.v) & 15) == 0);  // TMA needs 16-B aligned pools
+}
+
+// Split-K plan: one CTA per (KV head, request) when that already fills the resident CTA
+// slots (occupancy x SMs); otherwise split each item's tiles so the launch is close to one
+// full wave, keeping >= 2 tiles (128 slots) per split.  A pure function of the shapes, so
+// trie_attn_scratch_bytes and trie_attn_decode agree.
+int attn_plan_splits(const AttnParams& p, int rows_est, int sms) {
+  const int units = p.R * p.Hkv;
+  int occ = 2;
+  if (tc_shape_ok(p)) {
+    const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv));
+    if (k) occ = k->occ;
+  }
+  const int slots = occ * sms;
+  if (units >= slots) return 1;
+  int splits = slots / units;
+  const int max_by_rows = rows_est / 128 > 0 ? rows_est / 128 : 1;
+  if (splits > max_by_rows) splits = max_by_rows;
+  if (splits > 64) splits = 64;
+  return splits < 1 ? 1 : splits;
 }
 
 int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
-  switch (p.D) {
-    case 64: return launch_d<64>(p, s);
-    case 96: return launch_d<96>(p, s);
-    case 128: return launch_d<128>(p, s);
-  }
-  return trie_set_error(TRIE_EINVAL, "tensor-core attention: unsupported head_dim %d", p.D);
+  const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv));
+  if (!k) return trie_set_error(TRIE_EINVAL, "tensor-core attention: unsupported head_dim %d", p.D);
+  CUtensorMap km, vm;
+  const long rows = (long)p.R * p.Hkv * p.cap;
+  int rc = cached_map(&km, p.k, p.D, rows);
+  if (!rc) rc = cached_map(&vm, p.v, p.D, rows);
+  if (rc) return rc;
+  AttnParams pp = p;
+  void* args[3] = {(void*)&km, (void*)&vm, (void*)&pp};
+  cudaLaunchKernel(k->fn, dim3(p.Hkv, p.R, p.splits), dim3(k->threads), args, (size_t)k->smem, s);
+  rc = trie_check_launch("k_attn_tc");
+  if (rc) return rc;
+  if (p.splits > 1) rc = launch_attn_combine_bf16(p, s);
+  return rc;
 }
 
 }  // namespace trie
