@@ -220,15 +220,14 @@ static trie::AttnParams shape_params(const trie_cfg* cfg, int b_live) {
   return p;
 }
 
-static int attn_splits(const trie_cfg* c, int b_live, int rows_hint) {
-  const int rows = rows_hint > 0 ? rows_hint : c->capacity;
+static int sm_count() {
   static int sm_cache[64] = {0};
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess && dev < 64) {
     if (!sm_cache[dev]) cudaDeviceGetAttribute(&sm_cache[dev], cudaDevAttrMultiProcessorCount, dev);
     if (sm_cache[dev]) sms = sm_cache[dev];
   }
-  return trie::attn_plan_splits(shape_params(c, b_live), rows, sms);
+  return sms;
 }
 
 static size_t part_bytes(const trie_cfg* c, int b_live, int splits) {
@@ -237,12 +236,36 @@ static size_t part_bytes(const trie_cfg* c, int b_live, int splits) {
   return (size_t)c->n_requests * c->n_kv_heads * splits * Qg * (c->head_dim + 2) * 4;
 }
 
+// Attention plan: persistent tensor-core path (default for bf16, D in {64, 96, 128},
+// b_live*g <= 128) or the per-item paths; split count; scratch layout
+// [queue/item counters | split partials | derived beam mask].  A pure function of the
+// shapes, so trie_attn_scratch_bytes and trie_attn_decode agree.
+struct AttnPlan {
+  bool persist;
+  int splits;
+  size_t counter_bytes, part_bytes, mask_bytes;
+};
+
+static AttnPlan attn_plan(const trie_cfg* c, int b_live, int rows_hint) {
+  AttnPlan pl{};
+  const int rows = rows_hint > 0 ? rows_hint : c->capacity;
+  const trie::AttnParams sp = shape_params(c, b_live);
+  pl.persist = trie::attn_persist_enabled() && trie::attn_tc_shape_ok(sp);
+  if (pl.persist) {
+    pl.splits = trie::attn_persist_splits(sp, rows, sm_count());
+    pl.counter_bytes = align_up(trie::attn_persist_counter_bytes(sp));
+  } else {
+    pl.splits = trie::attn_plan_splits(sp, rows, sm_count());
+  }
+  pl.part_bytes = align_up(part_bytes(c, b_live, pl.splits));
+  pl.mask_bytes = align_up((size_t)c->n_requests * c->capacity * 4);
+  return pl;
+}
+
 size_t trie_attn_scratch_bytes(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint) {
   if (validate(cfg)) return 0;
-  const int splits = attn_splits(cfg, b_live, rows_hint);
-  // split partials + a derived beam_mask when the caller passes none
-  return align_up(part_bytes(cfg, b_live, splits)) +
-         align_up((size_t)cfg->n_requests * cfg->capacity * 4) + 256;
+  const AttnPlan pl = attn_plan(cfg, b_live, rows_hint);
+  return pl.counter_bytes + pl.part_bytes + pl.mask_bytes + 256;
 }
 
 int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const void* k_pool,
@@ -256,10 +279,9 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
   if (!q || !k_pool || !v_pool || !prompt_len || !depth || !leaf_ids || !n_nodes || !out)
     return trie_set_error(TRIE_EINVAL, "null argument");
   if (window < 0) return trie_set_error(TRIE_EINVAL, "window < 0");
-  const int splits = attn_splits(cfg, b_live, rows_hint);
-  const size_t pb = align_up(part_bytes(cfg, b_live, splits));
-  const size_t mb = align_up((size_t)cfg->n_requests * cfg->capacity * 4);
-  const size_t need = pb + (beam_mask ? 0 : mb);
+  const AttnPlan pl = attn_plan(cfg, b_live, rows_hint);
+  const size_t pb = pl.counter_bytes + pl.part_bytes;
+  const size_t need = pb + (beam_mask ? 0 : pl.mask_bytes);
   if (need > 0 && (!scratch || scratch_bytes < need))
     return trie_set_error(TRIE_ECAPACITY, "attention scratch %zu < %zu", scratch_bytes, need);
   if (!beam_mask) {
@@ -281,11 +303,13 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
   p.leaf = leaf_ids;
   p.nn = n_nodes;
   p.mask = beam_mask;
-  p.part = (float*)scratch;
+  p.aux = scratch;
+  p.part = (float*)((char*)scratch + pl.counter_bytes);
   p.status = nullptr;
   p.window = window;
-  p.splits = splits;
-  if (trie::attn_tc_supported(p)) return trie::launch_attn_tc(p, stream);
+  p.splits = pl.splits;
+  if (trie::attn_tc_supported(p))
+    return pl.persist ? trie::launch_attn_persist(p, stream) : trie::launch_attn_tc(p, stream);
   return trie::launch_attn_v1(p, stream);
 }
 

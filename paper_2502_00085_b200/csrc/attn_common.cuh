@@ -16,6 +16,7 @@ struct AttnParams {
   const int32_t* nn;      // [R]
   const uint32_t* mask;   // [R][cap]
   float* part;            // split partials
+  void* aux;              // persistent path: zero-initialised queue / item counters
   uint32_t* status;
   int R, b_live, Hq, Hkv, D, cap, window, splits;
   float scale_log2;       // log2(e) / sqrt(D)
@@ -27,5 +28,10 @@ int launch_attn_tc(const AttnParams& p, cudaStream_t s);
 bool attn_tc_supported(const AttnParams& p);
 int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s);
 int attn_plan_splits(const AttnParams& p, int rows_est, int sms);
+bool attn_persist_enabled();
+bool attn_tc_shape_ok(const AttnParams& p);
+int attn_persist_splits(const AttnParams& p, int rows_est, int sms);
+size_t attn_persist_counter_bytes(const AttnParams& p);
+int launch_attn_persist(const AttnParams& p, cudaStream_t s);
 
 }  // namespace trie

@@ -30,164 +30,9 @@
 #include "attn_common.cuh"
 #include "common.cuh"
 #include "handle.h"
+#include "tc_common.cuh"
 
 namespace trie {
-
-constexpr int TC_TR = 64;  // slots per tile
-constexpr int TC_CW = 32;  // elements per swizzle box column (64 bytes, SWIZZLE_64B)
-
-// ---- PTX helpers -------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void* src, uint32_t bytes,
-                                             uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(dst),
-      "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c,
-                                        uint32_t& d) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c,
-                                          uint32_t& d) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
-               : "r"(addr));
-}
-__device__ __forceinline__ uint32_t movm_t(uint32_t a) {
-  uint32_t d;
-  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
-  return d;
-}
-__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                         uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *(uint32_t*)&v;
-}
-
-// byte offset of (row, col) inside one tile: D/32 boxes of [TR rows][32 cols], 64B swizzle
-// (CUTLASS Swizzle<2,4,3>: address bits [4,5] ^= bits [7,8]; boxes are 1024-B aligned)
-__device__ __forceinline__ uint32_t tile_off(int row, int col) {
-  const int box = col / TC_CW;
-  const uint32_t o = (uint32_t)row * 64u + (uint32_t)(col % TC_CW) * 2u;
-  return (uint32_t)box * (TC_TR * 64u) + (o ^ (((o >> 7) & 3u) << 4));
-}
-
-template <int D, int STAGES_>
-struct Ring {
-  static constexpr int STAGES = STAGES_;
-  static constexpr int TILE_BYTES = TC_TR * D * 2;
-  // stage = K tile | V tile | mask words | depth words, 1024-byte aligned (swizzle atoms)
-  static constexpr int STAGE_BYTES = (2 * TILE_BYTES + 2 * TC_TR * 4 + 1023) / 1024 * 1024;
-  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
-};
-
-struct ItemInfo {
-  int tile0, ntiles, lo, N, t, fast_from;
-};
-
-// Thread 0: tile range of this (r, split) and the first tile index from which the mask
-// is needed (tiles below it are prompt-only and inside every beam's window).
-__device__ __forceinline__ void item_setup(const AttnParams& p, int r, int split, ItemInfo* info) {
-  const size_t mbase = (size_t)r * p.cap;
-  const int N = p.nn[r], t = p.tlen[r];
-  int lo = 0, lo_dep_max = INT_MIN;
-  if (p.window > 0) {
-    int lo_dep = INT_MAX;
-    for (int j = 0; j < p.b_live; ++j) {
-      const int d = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + j]] - p.window + 1;
-      lo_dep = min(lo_dep, d);
-      lo_dep_max = max(lo_dep_max, d);
-    }
-    int a = 0, b = N;  // first slot with depth >= lo_dep (depth non-decreasing)
-    while (a < b) {
-      const int mid = (a + b) >> 1;
-      if (p.depth[mbase + mid] < lo_dep) a = mid + 1; else b = mid;
-    }
-    lo = a;
-  }
-  const int first = lo / TC_TR;
-  const int total = (N + TC_TR - 1) / TC_TR - first;
-  const int per = (total + p.splits - 1) / p.splits;
-  const int tb = min(total, split * per), te = min(total, (split + 1) * per);
-  info->tile0 = first + tb;
-  info->ntiles = te - tb;
-  info->lo = lo;
-  info->N = N;
-  info->t = t;
-  // unmasked tiles: every row n satisfies n < t (prompt: depth = n), n < N and
-  // depth = n >= every beam's lower depth  <=>  tile in [ceil(lo_dep_max / TR), t / TR)
-  const int fmin = p.window > 0 ? (max(lo_dep_max, 0) + TC_TR - 1) / TC_TR : 0;
-  info->fast_from = fmin;  // fast tiles: fmin <= tile < min(t, N) / TR
-}
-
-template <int D, int STAGES>
-__device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUtensorMap* vmap,
-                                              const AttnParams& p, int r, int h,
-                                              const ItemInfo& it, uint8_t* ring, uint64_t* full,
-                                              uint64_t* empty) {
-  using RG = Ring<D, STAGES>;
-  const int row_base = (r * p.Hkv + h) * p.cap;
-  const size_t mbase = (size_t)r * p.cap;
-  for (int i = 0; i < it.ntiles; ++i) {
-    const int s = i % STAGES;
-    const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-    mbar_wait(&empty[s], ph ^ 1u);
-    const uint32_t st = smem_u32(ring + s * RG::STAGE_BYTES);
-    const int n0 = (it.tile0 + i) * TC_TR;
-    // mask / depth words clamped to the [R][cap] arrays (cap % 4 == 0: 16-byte granules)
-    const uint32_t mdb = (uint32_t)min(TC_TR, p.cap - n0) * 4u;
-    mbar_expect_tx(&full[s], 2 * RG::TILE_BYTES + 2 * mdb);
-#pragma unroll
-    for (int bx = 0; bx < D / TC_CW; ++bx) {
-      tma_load_2d(st + bx * TC_TR * 64, kmap, bx * TC_CW, row_base + n0, &full[s]);
-      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vmap, bx * TC_CW, row_base + n0, &full[s]);
-    }
-    bulk_load_1d(st + 2 * RG::TILE_BYTES, p.mask + mbase + n0, mdb, &full[s]);
-    bulk_load_1d(st + 2 * RG::TILE_BYTES + TC_TR * 4, p.depth + mbase + n0, mdb, &full[s]);
-  }
-}
 
 // =========================================================================================
 // narrow: Qg <= 8 * NQ (NQ in {1, 2}); CTA = producer warp + one consumer warp
@@ -714,7 +559,7 @@ struct MapEntry {
   int D;
   CUtensorMap map;
 };
-static int cached_map(CUtensorMap* out, const void* base, int D, long rows) {
+int cached_tensor_map(CUtensorMap* out, const void* base, int D, long rows) {
   static MapEntry cache[512];
   const size_t slot = (((uintptr_t)base >> 8) ^ ((uintptr_t)base >> 20)) % 512;
   MapEntry& e = cache[slot];
@@ -796,13 +641,13 @@ static const TcKernel* select_tc(int D, int Qg) {
   return nullptr;
 }
 
-static bool tc_shape_ok(const AttnParams& p) {
+bool attn_tc_shape_ok(const AttnParams& p) {
   const int Qg = p.b_live * (p.Hq / p.Hkv);
   return p.bf16 && Qg <= 128 && p.cap % 4 == 0 && (p.D == 64 || p.D == 96 || p.D == 128);
 }
 
 bool attn_tc_supported(const AttnParams& p) {
-  if (!tc_shape_ok(p)) return false;
+  if (!attn_tc_shape_ok(p)) return false;
   return ((((uintptr_t)p.k | (uintptr_t)p.v) & 15) == 0);  // TMA needs 16-B aligned pools
 }
 
@@ -813,7 +658,7 @@ bool attn_tc_supported(const AttnParams& p) {
 int attn_plan_splits(const AttnParams& p, int rows_est, int sms) {
   const int units = p.R * p.Hkv;
   int occ = 2;
-  if (tc_shape_ok(p)) {
+  if (attn_tc_shape_ok(p)) {
     const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv));
     if (k) occ = k->occ;
   }
@@ -831,8 +676,8 @@ int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
   if (!k) return trie_set_error(TRIE_EINVAL, "tensor-core attention: unsupported head_dim %d", p.D);
   CUtensorMap km, vm;
   const long rows = (long)p.R * p.Hkv * p.cap;
-  int rc = cached_map(&km, p.k, p.D, rows);
-  if (!rc) rc = cached_map(&vm, p.v, p.D, rows);
+  int rc = cached_tensor_map(&km, p.k, p.D, rows);
+  if (!rc) rc = cached_tensor_map(&vm, p.v, p.D, rows);
   if (rc) return rc;
   AttnParams pp = p;
   void* args[3] = {(void*)&km, (void*)&vm, (void*)&pp};

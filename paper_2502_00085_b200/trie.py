@@ -77,7 +77,9 @@ class TrieState:
         b_live = self.b_live
         need = L.trie_attn_scratch_bytes(self.cfg, b_live, rows_hint)
         if self.attn_scratch is None or self.attn_scratch.numel() < need:
-            self.attn_scratch = torch.empty(need, dtype=torch.uint8, device=self.device)
+            # zero-initialised once: the persistent kernel's queue counters live here and
+            # every launch leaves them at zero
+            self.attn_scratch = torch.zeros(need, dtype=torch.uint8, device=self.device)
         L.trie_attn_decode(self.cfg, b_live, q, k_pool_l, v_pool_l, self.prompt_len, self.parent,
                            self.depth, self.leaf, self.n_nodes, self.beam_mask if use_mask else None,
                            self.window, rows_hint, out, lse, self.attn_scratch, stream)
