@@ -703,7 +703,7 @@ bool attn_persist_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("TRIE_ATTN_PERSIST");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : 0;  // opt-in (r04: slower than the per-item path)
   }
   return v != 0;
 }
