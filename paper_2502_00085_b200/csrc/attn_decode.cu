@@ -201,13 +201,26 @@ __global__ void k_attn_combine(const AttnParams p) {
   float acc[8];
 #pragma unroll
   for (int c = 0; c < 8; ++c) acc[c] = 0.f;
-  for (int s = 0; s < p.splits; ++s) {
-    const float w = __shfl_sync(0xffffffffu, ws[s >> 5], s & 31);
-    if (w == 0.f) continue;  // uniform
-    const float* pp = base + ((size_t)s * Qg + m) * (D + 2);
+  // batches of 4 splits: all loads of a batch are issued before any is consumed
+  constexpr int SB = 4;
+  for (int s0 = 0; s0 < p.splits; s0 += SB) {
+    float v[SB][8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (lane + 32 * c < D) acc[c] += w * pp[lane + 32 * c];
+    for (int u = 0; u < SB; ++u) {
+      const int s = s0 + u;
+      const float* pp = base + ((size_t)min(s, p.splits - 1) * Qg + m) * (D + 2);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[u][c] = (lane + 32 * c < D) ? __ldg(pp + lane + 32 * c) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < SB; ++u) {
+      const int s = s0 + u;
+      const float w = __shfl_sync(0xffffffffu, ws[(s >> 5) & 1], s & 31);
+      if (s < p.splits) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] += w * v[u][c];
+      }
+    }
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c)
