@@ -304,22 +304,29 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
 // =========================================================================================
 // wide: 16 < Qg <= 16 * MT; CTA = producer warp + MT consumer warps (one query m-tile each)
 // =========================================================================================
-template <int D, int MT>
+template <int D, int MT, int RS = 1>
 struct WideCfg {
   static constexpr int STAGES = D >= 128 ? 3 : 4;
   using RG = Ring<D, STAGES>;
   static constexpr int KS = D / 16;
   static constexpr int DT = D / 8;
-  static constexpr int NT = TC_TR / 8;  // S n-tiles per tile
+  static constexpr int RSZ = TC_TR / RS;  // tile rows per warp
+  static constexpr int NT = RSZ / 8;      // S n-tiles per warp
+  static constexpr int NC = MT * RS;      // consumer warps
+  static_assert(NT % 2 == 0, "row slice must be a multiple of 16");
+  static_assert((RS - 1) * MT * 16 * (D + 2) * 4 <= RG::RING_BYTES, "merge buffer must fit the ring");
   static constexpr int SMEM = RG::RING_BYTES + 2 * STAGES * 8 + 64 + 1024;
-  static constexpr int THREADS = 32 * (MT + 1);
+  static constexpr int THREADS = 32 * (NC + 1);
 };
 
-template <int D, int MT>
-__global__ void __launch_bounds__(WideCfg<D, MT>::THREADS) k_attn_wide(
+// Warp (mt, rs) owns query m-tile mt (16 queries) and rows [rs*RSZ, (rs+1)*RSZ) of every
+// tile; with RS > 1 the row slices of an m-tile are merged once, at the end, through the
+// (drained) ring.  S = Q K^T with two independent n-tiles per ldmatrix.x4.
+template <int D, int MT, int RS>
+__global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p) {
-  using C = WideCfg<D, MT>;
+  using C = WideCfg<D, MT, RS>;
   using RG = typename C::RG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT>::THREADS) k_attn_wide(
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MT);
+      mbar_init(&empty[s], C::NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     item_setup(p, r, split, info);
@@ -344,7 +351,9 @@ __global__ void __launch_bounds__(WideCfg<D, MT>::THREADS) k_attn_wide(
     if (lane == 0) producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
     return;
   }
-  const int mt = warp - 1;
+  const int cw = warp - 1;
+  const int mt = cw % MT, rs = cw / MT;
+  const int r0 = rs * C::RSZ;
   const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
   const int gq = lane >> 2, cq = lane & 3;
   const size_t mbase = (size_t)r * p.cap;
@@ -357,7 +366,6 @@ __global__ void __launch_bounds__(WideCfg<D, MT>::THREADS) k_attn_wide(
     if (p.window > 0 && qm[u] < Qg)
       lod[u] = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam[u]]] - p.window + 1;
   }
-  // Q fragments (A operand, row-major 16 x D), zero for padded queries
   uint32_t qa[C::KS][4];
   {
     const __nv_bfloat16* qb = (const __nv_bfloat16*)p.q;
@@ -379,7 +387,6 @@ __global__ void __launch_bounds__(WideCfg<D, MT>::THREADS) k_attn_wide(
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   const float sc = p.scale_log2;
   const int fast_end = min(it.t, it.N) / TC_TR;
-  const bool active = mt * 16 < Qg;  // (MT is the smallest that covers Qg: always true)
 
   for (int i = 0; i < it.ntiles; ++i) {
     const int s = i % C::STAGES;
@@ -389,97 +396,96 @@ __global__ void __launch_bounds__(WideCfg<D, MT>::THREADS) k_attn_wide(
     const int tile = it.tile0 + i;
     const int n0 = tile * TC_TR;
     const bool fast = tile >= it.fast_from && tile < fast_end;
-    if (active) {
-      float sacc[C::NT][4];
+    float sacc[C::NT][4];
 #pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+    for (int nt = 0; nt < C::NT; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
 #pragma unroll
-      for (int ks = 0; ks < C::KS; ks += 2)
+    for (int ks = 0; ks < C::KS; ++ks)
 #pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt) {
-          const int row = nt * 8 + (lane & 7);
-          const int col = ks * 16 + (lane >> 3) * 8;
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(kbase + tile_off(row, col), b0, b1, b2, b3);
-          mma_bf16(sacc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-          mma_bf16(sacc[nt], qa[ks + 1][0], qa[ks + 1][1], qa[ks + 1][2], qa[ks + 1][3], b2, b3);
-        }
-      float tmax[2] = {-INFINITY, -INFINITY};
-      if (fast) {
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int u = e >> 1;
-            const float v = qm[u] < Qg ? sacc[nt][e] * sc : -INFINITY;
-            sacc[nt][e] = v;
-            tmax[u] = fmaxf(tmax[u], v);
-          }
-      } else {
-        const uint32_t* tmask = (const uint32_t*)(st + 2 * RG::TILE_BYTES);
-        const int* tdep = (const int*)(st + 2 * RG::TILE_BYTES + TC_TR * 4);
-#pragma unroll
-        for (int nt = 0; nt < C::NT; ++nt)
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            const int lr = nt * 8 + cq * 2 + cc;
-            const int n = n0 + lr;
-            const bool rowin = n < it.N;
-            const uint32_t mw = rowin ? tmask[lr] : 0u;
-            const int dep = rowin ? tdep[lr] : INT_MIN;
-            const bool prompt = n < it.t;
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const bool ok = rowin && qm[u] < Qg && (prompt || ((mw >> beam[u]) & 1u)) && dep >= lod[u];
-              const float v = ok ? sacc[nt][u * 2 + cc] * sc : -INFINITY;
-              sacc[nt][u * 2 + cc] = v;
-              tmax[u] = fmaxf(tmax[u], v);
-            }
-          }
+      for (int nt = 0; nt < C::NT; nt += 2) {
+        // x4: (n-tile nt, k lo), (nt, k hi), (nt+1, k lo), (nt+1, k hi)
+        const int row = r0 + (nt + (lane >> 4)) * 8 + (lane & 7);
+        const int col = ks * 16 + ((lane >> 3) & 1) * 8;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kbase + tile_off(row, col), b0, b1, b2, b3);
+        mma_bf16(sacc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+        mma_bf16(sacc[nt + 1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
       }
-      float alpha[2];
+    float tmax[2] = {-INFINITY, -INFINITY};
+    if (fast) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 1));
-        tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 2));
-        const float mnew = fmaxf(mrow[u], tmax[u]);
-        alpha[u] = (mnew == -INFINITY) ? 1.f : exp2f(mrow[u] - mnew);
-        mrow[u] = mnew;
-        lrow[u] *= alpha[u];
-      }
-      uint32_t pa[C::NT][2];
-#pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt) {
-        float pv[4];
+      for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int u = e >> 1;
-          pv[e] = (sacc[nt][e] == -INFINITY) ? 0.f : exp2f(sacc[nt][e] - mrow[u]);
-          lrow[u] += pv[e];
+          const float v = qm[u] < Qg ? sacc[nt][e] * sc : -INFINITY;
+          sacc[nt][e] = v;
+          tmax[u] = fmaxf(tmax[u], v);
         }
-        pa[nt][0] = pack_bf16(pv[0], pv[1]);
-        pa[nt][1] = pack_bf16(pv[2], pv[3]);
-      }
+    } else {
+      const uint32_t* tmask = (const uint32_t*)(st + 2 * RG::TILE_BYTES);
+      const int* tdep = (const int*)(st + 2 * RG::TILE_BYTES + TC_TR * 4);
 #pragma unroll
-      for (int dt = 0; dt < C::DT; ++dt) {
-        o[dt][0] *= alpha[0];
-        o[dt][1] *= alpha[0];
-        o[dt][2] *= alpha[1];
-        o[dt][3] *= alpha[1];
-      }
+      for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-      for (int kc = 0; kc < C::NT / 2; ++kc) {
-        const uint32_t a0 = pa[2 * kc][0], a1 = pa[2 * kc][1], a2 = pa[2 * kc + 1][0],
-                       a3 = pa[2 * kc + 1][1];
+        for (int cc = 0; cc < 2; ++cc) {
+          const int lr = r0 + nt * 8 + cq * 2 + cc;
+          const int n = n0 + lr;
+          const bool rowin = n < it.N;
+          const uint32_t mw = rowin ? tmask[lr] : 0u;
+          const int dep = rowin ? tdep[lr] : INT_MIN;
+          const bool prompt = n < it.t;
 #pragma unroll
-        for (int dt = 0; dt < C::DT; dt += 2) {
-          const int row = kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-          const int col = dt * 8 + (lane >> 4) * 8;
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(vbase + tile_off(row, col), b0, b1, b2, b3);
-          mma_bf16(o[dt], a0, a1, a2, a3, b0, b1);
-          mma_bf16(o[dt + 1], a0, a1, a2, a3, b2, b3);
+          for (int u = 0; u < 2; ++u) {
+            const bool ok = rowin && qm[u] < Qg && (prompt || ((mw >> beam[u]) & 1u)) && dep >= lod[u];
+            const float v = ok ? sacc[nt][u * 2 + cc] * sc : -INFINITY;
+            sacc[nt][u * 2 + cc] = v;
+            tmax[u] = fmaxf(tmax[u], v);
+          }
         }
+    }
+    float alpha[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 1));
+      tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 2));
+      const float mnew = fmaxf(mrow[u], tmax[u]);
+      alpha[u] = (mnew == -INFINITY) ? 1.f : exp2f(mrow[u] - mnew);
+      mrow[u] = mnew;
+      lrow[u] *= alpha[u];
+    }
+    uint32_t pa[C::NT][2];
+#pragma unroll
+    for (int nt = 0; nt < C::NT; ++nt) {
+      float pv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int u = e >> 1;
+        pv[e] = (sacc[nt][e] == -INFINITY) ? 0.f : exp2f(sacc[nt][e] - mrow[u]);
+        lrow[u] += pv[e];
+      }
+      pa[nt][0] = pack_bf16(pv[0], pv[1]);
+      pa[nt][1] = pack_bf16(pv[2], pv[3]);
+    }
+#pragma unroll
+    for (int dt = 0; dt < C::DT; ++dt) {
+      o[dt][0] *= alpha[0];
+      o[dt][1] *= alpha[0];
+      o[dt][2] *= alpha[1];
+      o[dt][3] *= alpha[1];
+    }
+#pragma unroll
+    for (int kc = 0; kc < C::NT / 2; ++kc) {
+      const uint32_t a0 = pa[2 * kc][0], a1 = pa[2 * kc][1], a2 = pa[2 * kc + 1][0],
+                     a3 = pa[2 * kc + 1][1];
+#pragma unroll
+      for (int dt = 0; dt < C::DT; dt += 2) {
+        const int row = r0 + kc * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int col = dt * 8 + (lane >> 4) * 8;
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vbase + tile_off(row, col), b0, b1, b2, b3);
+        mma_bf16(o[dt], a0, a1, a2, a3, b0, b1);
+        mma_bf16(o[dt + 1], a0, a1, a2, a3, b2, b3);
       }
     }
     __syncwarp();
@@ -489,6 +495,51 @@ __global__ void __launch_bounds__(WideCfg<D, MT>::THREADS) k_attn_wide(
   for (int u = 0; u < 2; ++u) {
     lrow[u] += __shfl_xor_sync(0xffffffffu, lrow[u], 1);
     lrow[u] += __shfl_xor_sync(0xffffffffu, lrow[u], 2);
+  }
+  if constexpr (RS > 1) {
+    // row-slice merge: slices rs > 0 park (O, m, l) in the drained ring, slice 0 folds them
+    asm volatile("bar.sync 1, %0;" ::"r"(C::NC * 32));
+    float* red = (float*)smem;  // [(RS-1) * MT][16][D + 2]
+    constexpr int RW = D + 2;
+    if (rs > 0) {
+      float* mine = red + (size_t)((rs - 1) * MT + mt) * 16 * RW;
+#pragma unroll
+      for (int dt = 0; dt < C::DT; ++dt) {
+        const int col = dt * 8 + cq * 2;
+        mine[gq * RW + col] = o[dt][0];
+        mine[gq * RW + col + 1] = o[dt][1];
+        mine[(gq + 8) * RW + col] = o[dt][2];
+        mine[(gq + 8) * RW + col + 1] = o[dt][3];
+      }
+      if (cq == 0) {
+        mine[gq * RW + D] = mrow[0];
+        mine[gq * RW + D + 1] = lrow[0];
+        mine[(gq + 8) * RW + D] = mrow[1];
+        mine[(gq + 8) * RW + D + 1] = lrow[1];
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(C::NC * 32));
+    if (rs > 0) return;
+#pragma unroll
+    for (int x = 0; x < RS - 1; ++x) {
+      const float* src = red + (size_t)(x * MT + mt) * 16 * RW;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int row = gq + 8 * u;
+        const float m2 = src[row * RW + D], l2 = src[row * RW + D + 1];
+        const float mn = fmaxf(mrow[u], m2);
+        const float w1 = mrow[u] == -INFINITY ? 0.f : exp2f(mrow[u] - mn);
+        const float w2 = m2 == -INFINITY ? 0.f : exp2f(m2 - mn);
+#pragma unroll
+        for (int dt = 0; dt < C::DT; ++dt) {
+          const int col = dt * 8 + cq * 2;
+          o[dt][u * 2] = o[dt][u * 2] * w1 + src[row * RW + col] * w2;
+          o[dt][u * 2 + 1] = o[dt][u * 2 + 1] * w1 + src[row * RW + col + 1] * w2;
+        }
+        lrow[u] = lrow[u] * w1 + l2 * w2;
+        mrow[u] = mn;
+      }
+    }
   }
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
@@ -597,10 +648,30 @@ static const TcKernel& narrow_k() {
   static const TcKernel k = make_tc(k_attn_narrow<D, NQ, ST>, NarrowCfg<D, NQ, ST>::SMEM, 64);
   return k;
 }
-template <int D, int MT>
+template <int D, int MT, int RS>
 static const TcKernel& wide_k() {
-  static const TcKernel k = make_tc(k_attn_wide<D, MT>, WideCfg<D, MT>::SMEM, WideCfg<D, MT>::THREADS);
+  static const TcKernel k =
+      make_tc(k_attn_wide<D, MT, RS>, WideCfg<D, MT, RS>::SMEM, WideCfg<D, MT, RS>::THREADS);
   return k;
+}
+// row slices per wide tile (TRIE_WIDE_RS in {1, 2, 4}; default 2: two warps per query
+// m-tile so each SM scheduler has more than one warp to switch to)
+static int wide_rs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TRIE_WIDE_RS");
+    v = e ? atoi(e) : 2;
+    if (v != 1 && v != 2 && v != 4) v = 2;
+  }
+  return v;
+}
+template <int D, int MT>
+static const TcKernel& wide_sel() {
+  switch (wide_rs()) {
+    case 1: return wide_k<D, MT, 1>();
+    case 4: return wide_k<D, MT, (MT <= 2 ? 4 : 2)>();
+    default: return wide_k<D, MT, (MT <= 4 ? 2 : 1)>();
+  }
 }
 
 // Stages per narrow CTA (tuning knob TRIE_NARROW_STAGES in {2, 3, 4}).  Default 2: at
@@ -628,9 +699,9 @@ template <int D>
 static const TcKernel& select_d(int Qg) {
   if (Qg <= 8) return narrow_sel<D, 1>();
   if (Qg <= 16) return narrow_sel<D, 2>();
-  if (Qg <= 32) return wide_k<D, 2>();
-  if (Qg <= 64) return wide_k<D, 4>();
-  return wide_k<D, 8>();
+  if (Qg <= 32) return wide_sel<D, 2>();
+  if (Qg <= 64) return wide_sel<D, 4>();
+  return wide_sel<D, 8>();
 }
 static const TcKernel* select_tc(int D, int Qg) {
   switch (D) {
