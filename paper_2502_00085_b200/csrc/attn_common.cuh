@@ -30,6 +30,9 @@ int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s);
 int attn_plan_splits(const AttnParams& p, int rows_est, int sms);
 bool attn_persist_enabled();
 bool attn_tc_shape_ok(const AttnParams& p);
+bool attn_umma_eligible(const AttnParams& p);
+int attn_umma_occ(const AttnParams& p);
+int launch_attn_umma(const AttnParams& p, cudaStream_t s);
 int attn_persist_splits(const AttnParams& p, int rows_est, int sms);
 size_t attn_persist_counter_bytes(const AttnParams& p);
 int launch_attn_persist(const AttnParams& p, cudaStream_t s);

@@ -729,7 +729,9 @@ bool attn_tc_supported(const AttnParams& p) {
 int attn_plan_splits(const AttnParams& p, int rows_est, int sms) {
   const int units = p.R * p.Hkv;
   int occ = 2;
-  if (attn_tc_shape_ok(p)) {
+  if (attn_umma_eligible(p)) {
+    occ = attn_umma_occ(p);
+  } else if (attn_tc_shape_ok(p)) {
     const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv));
     if (k) occ = k->occ;
   }
@@ -743,6 +745,7 @@ int attn_plan_splits(const AttnParams& p, int rows_est, int sms) {
 }
 
 int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
+  if (attn_umma_eligible(p)) return launch_attn_umma(p, s);
   const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv));
   if (!k) return trie_set_error(TRIE_EINVAL, "tensor-core attention: unsupported head_dim %d", p.D);
   CUtensorMap km, vm;

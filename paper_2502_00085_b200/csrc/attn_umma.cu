@@ -1,0 +1,433 @@
+// trie_attn_decode, tcgen05 / TMEM path for wide query groups (sm_100a).
+// §3.3: o = softmax(q K^T / sqrt(D)) V over each beam's root-to-leaf rows.
+//
+// When b_live x (Hq/Hkv) >= 33 queries share a KV head, the legacy mma.sync path becomes
+// tensor-pipe bound (r05: b=16, g=4 at 8k context stalls at ~3.2 TB/s).  Here one thread
+// issues 5th-generation tensor-core MMAs with the accumulators in tensor memory:
+//   S[128 x 64] = Q[128 x D] . K_tile^T      (A = Q in smem, K-major SW64; B = the TMA
+//                                             K tile, K-major SW64; fp32 in TMEM)
+//   O[128 x D] += P[128 x 64] . V_tile        (A = P in TMEM, bf16; B = the TMA V tile,
+//                                             MN-major SW64; fp32 in TMEM)
+// The TMA tiles written by the producer ARE the canonical UMMA layouts (64-byte rows,
+// 8-row atoms of 512 B, 32-column boxes 4096 B apart), so no re-staging is needed.
+// Warp roles: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..5 = softmax /
+// epilogue (warp w reads TMEM lanes 32*(w%4).., thread = query row).  S is double
+// buffered so QK of tile i+1 overlaps the softmax of tile i; the running max is rescaled
+// lazily (O is only rescaled when a row max grows by > 8 in log2 units).
+// Rows >= Qg of the 128-row MMA are padding (Q rows zero, P rows zero, outputs ignored).
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "attn_common.cuh"
+#include "common.cuh"
+#include "handle.h"
+#include "tc_common.cuh"
+
+namespace trie {
+
+// ---- tcgen05 PTX helpers ----------------------------------------------------------------
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // version 1 (Blackwell)
+  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+  return d;
+}
+// kind::f16 instruction descriptor: fp32 accumulate, bf16 A and B
+__host__ __device__ constexpr uint32_t umma_idesc(int M, int N, int b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                        uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]),
+        "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+      "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+      "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int D, int ST>
+struct UCfg {
+  using RG = Ring<D, ST>;
+  static constexpr int STAGES = ST;
+  static constexpr int QBYTES = 128 * D * 2;  // Q: 128 rows (padding zero), D/32 boxes
+  static constexpr int OFF_Q = RG::RING_BYTES;
+  static constexpr int OFF_BAR = OFF_Q + QBYTES;
+  static constexpr int NBAR = 2 * ST + 2 + 2;  // full, empty, s_full[2], p_full, pv_done
+  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 64 + 1024;
+  static constexpr int THREADS = 6 * 32;
+  // TMEM columns: S0 [0,64), S1 [64,128), P [128,160), O [160, 160+D)
+  static constexpr int COL_S0 = 0, COL_S1 = 64, COL_P = 128, COL_O = 160;
+  static constexpr int TMEM_COLS = 512;
+  static_assert(COL_O + D <= TMEM_COLS, "TMEM budget");
+};
+
+template <int D, int ST>
+__global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
+    const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+    const AttnParams p) {
+  using C = UCfg<D, ST>;
+  using RG = typename C::RG;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ring = smem;
+  uint8_t* qsm = smem + C::OFF_Q;
+  uint64_t* full = (uint64_t*)(smem + C::OFF_BAR);
+  uint64_t* empty = full + ST;
+  uint64_t* s_full = empty + ST;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* pv_done = p_full + 1;
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + 1);
+  ItemInfo* info = (ItemInfo*)(tmem_slot + 4);
+
+  const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    item_setup(p, r, split, info);
+  }
+  if (warp == 1) {  // TMEM allocation (whole warp), address published through smem
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const ItemInfo it = *info;
+  const uint32_t tmem = *tmem_slot;
+  const int ntiles = it.ntiles;
+
+  if (warp == 0) {
+    if (lane == 0) producer_loop<D, ST>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    // wait for Q in smem (softmax warps) -- named barrier 1, 160 threads
+    asm volatile("bar.sync 1, 160;");
+    tc_fence_after();
+    const uint32_t idesc_qk = umma_idesc(128, 64, 0);
+    const uint32_t idesc_pv = umma_idesc(128, D, 1);
+    const uint32_t qbase = smem_u32(qsm);
+    auto issue_qk = [&](int i) {
+      const int s = i % ST;
+      mbar_wait(&full[s], (uint32_t)(i / ST) & 1u);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t kb = smem_u32(ring + s * RG::STAGE_BYTES);
+        const uint32_t d_s = tmem + ((i & 1) ? C::COL_S1 : C::COL_S0);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          // K step ks: box ks/2 (4096 B apart for the 64-row K tile, 16 KB for the 128-row Q),
+          // +32 B inside the 64-byte swizzle row for the odd half
+          const uint64_t a = umma_desc_sw64(qbase + (ks >> 1) * 128 * 64 + (ks & 1) * 32, 16, 512);
+          const uint64_t b = umma_desc_sw64(kb + (ks >> 1) * TC_TR * 64 + (ks & 1) * 32, 16, 512);
+          umma_ss(d_s, a, b, idesc_qk, ks > 0);
+        }
+        umma_commit(&s_full[i & 1]);
+      }
+      __syncwarp();
+    };
+    if (ntiles > 0) issue_qk(0);
+    for (int i = 0; i < ntiles; ++i) {
+      if (i + 1 < ntiles) issue_qk(i + 1);
+      mbar_wait(p_full, (uint32_t)i & 1u);
+      tc_fence_after();
+      if (lane == 0) {
+        const int s = i % ST;
+        const uint32_t vb = smem_u32(ring + s * RG::STAGE_BYTES + RG::TILE_BYTES);
+#pragma unroll
+        for (int kc = 0; kc < TC_TR / 16; ++kc) {
+          // V tile as MN-major B: 16 rows per K step = 2 atoms of 8 rows (1024 B); the
+          // 32-column boxes are LBO = 4096 B apart, 8-row atoms SBO = 512 B apart
+          const uint64_t b = umma_desc_sw64(vb + kc * 1024, TC_TR * 64, 512);
+          umma_ts(tmem + C::COL_O, tmem + C::COL_P + kc * 8, b, idesc_pv, (i > 0 || kc > 0) ? 1u : 0u);
+        }
+        umma_commit(&empty[s]);
+        umma_commit(pv_done);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ===================== softmax / epilogue warps (2..5) =====================
+    const int sp = warp & 3;                  // TMEM sub-partition of this warp
+    const int row = sp * 32 + lane;           // query row (MMA M index)
+    const int tid = threadIdx.x - 64;         // 0..127
+    // Q -> smem, 64B-swizzled K-major boxes of [128 rows][32 cols]; padding rows zero
+    {
+      const __nv_bfloat16* q = (const __nv_bfloat16*)p.q;
+      const int chunks = 128 * (D / 8);
+      for (int c = tid; c < chunks; c += 128) {
+        const int m = c / (D / 8), col = (c % (D / 8)) * 8;
+        int4 v = make_int4(0, 0, 0, 0);
+        if (m < Qg)
+          v = *(const int4*)(q + (((size_t)r * p.b_live + m / g) * p.Hq + h * g + m % g) * D + col);
+        const int box = col / TC_CW;
+        const uint32_t o = (uint32_t)m * 64u + (uint32_t)(col % TC_CW) * 2u;
+        *(int4*)(qsm + box * 128 * 64 + (o ^ (((o >> 7) & 3u) << 4))) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, 160;");
+    }
+    const bool qvalid = row < Qg;
+    const int beam = qvalid ? row / g : 0;
+    const size_t mbase = (size_t)r * p.cap;
+    const int lod = (p.window > 0 && qvalid) ? p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam]] - p.window + 1 : INT_MIN;
+    const float sc = p.scale_log2;
+    const int fast_end = min(it.t, it.N) / TC_TR;
+    const uint32_t lane_off = (uint32_t)(sp * 32) << 16;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int i = 0; i < ntiles; ++i) {
+      const int s = i % ST;
+      mbar_wait(&s_full[i & 1], (uint32_t)(i >> 1) & 1u);
+      mbar_wait(&full[s], (uint32_t)(i / ST) & 1u);  // (complete) makes the mask words visible
+      tc_fence_after();
+      uint32_t sv[64];
+      {
+        uint32_t a[32], b[32];
+        const uint32_t col = (i & 1) ? C::COL_S1 : C::COL_S0;
+        tmem_ld32(tmem + lane_off + col, a);
+        tmem_ld32(tmem + lane_off + col + 32, b);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          sv[k] = a[k];
+          sv[32 + k] = b[k];
+        }
+      }
+      const int tile = it.tile0 + i;
+      const int n0 = tile * TC_TR;
+      const bool fast = tile >= it.fast_from && tile < fast_end;
+      const uint8_t* stp = ring + s * RG::STAGE_BYTES;
+      const uint32_t* tmask = (const uint32_t*)(stp + 2 * RG::TILE_BYTES);
+      const int* tdep = (const int*)(stp + 2 * RG::TILE_BYTES + TC_TR * 4);
+      float tmax = -INFINITY;
+      float x[64];
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {
+        bool ok = qvalid;
+        if (!fast) {
+          const int n = n0 + k;
+          ok = ok && n < it.N && (n < it.t || ((tmask[k] >> beam) & 1u)) && tdep[k] >= lod;
+        }
+        x[k] = ok ? __uint_as_float(sv[k]) * sc : -INFINITY;
+        tmax = fmaxf(tmax, x[k]);
+      }
+      // lazy rescale: keep the running max unless the tile max exceeds it by > 8 (log2)
+      float alpha = 1.f;
+      bool rescale = false;
+      if (tmax > m_run + 8.f || (m_run == -INFINITY && tmax > -INFINITY)) {
+        const float mn = tmax;
+        alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mn);
+        rescale = m_run != -INFINITY;
+        m_run = mn;
+        l_run *= alpha;
+      }
+      uint32_t pk[32];
+      float psum = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const float p0 = x[2 * k] == -INFINITY ? 0.f : exp2f(x[2 * k] - m_run);
+        const float p1 = x[2 * k + 1] == -INFINITY ? 0.f : exp2f(x[2 * k + 1] - m_run);
+        psum += p0 + p1;
+        pk[k] = pack_bf16(p0, p1);
+      }
+      l_run += psum;
+      if (i > 0) {  // PV of the previous tile must be done before P / O are touched
+        mbar_wait(pv_done, (uint32_t)(i - 1) & 1u);
+        tc_fence_after();
+      }
+      if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_off + C::COL_O + c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+          tmem_st32(tmem + lane_off + C::COL_O + c, o);
+        }
+      }
+      tmem_st32(tmem + lane_off + C::COL_P, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // ---- epilogue: O / l ----
+    if (ntiles > 0) {
+      mbar_wait(pv_done, (uint32_t)(ntiles - 1) & 1u);
+      tc_fence_after();
+    }
+    const int j = beam, ii = row % g;
+    if (p.splits == 1) {
+      __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_off + C::COL_O + c, o);
+        tmem_wait_ld();
+        if (qvalid) {
+          uint32_t w[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            w[k] = pack_bf16(__uint_as_float(o[2 * k]) * inv, __uint_as_float(o[2 * k + 1]) * inv);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            *(int4*)(op + c + 8 * k) = make_int4((int)w[4 * k], (int)w[4 * k + 1], (int)w[4 * k + 2], (int)w[4 * k + 3]);
+        }
+      }
+      if (qvalid) {
+        if (l_run == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
+        if (p.lse)
+          p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
+              l_run > 0.f ? (m_run + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
+      }
+    } else {
+      float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + row) * (D + 2);
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_off + C::COL_O + c, o);
+        tmem_wait_ld();
+        if (qvalid) {
+#pragma unroll
+          for (int k = 0; k < 32; k += 4)
+            *(float4*)(pp + c + k) = make_float4(__uint_as_float(o[k]), __uint_as_float(o[k + 1]),
+                                                 __uint_as_float(o[k + 2]), __uint_as_float(o[k + 3]));
+        }
+      }
+      if (qvalid) {
+        pp[D] = m_run;
+        pp[D + 1] = l_run;
+      }
+    }
+  }
+  // teardown: everyone done with TMEM before the allocating warp frees it
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  }
+}
+
+// ---- host side ---------------------------------------------------------------------------
+int cached_tensor_map(CUtensorMap* out, const void* base, int D, long rows);
+
+struct UKernel {
+  const void* fn;
+  int smem, threads, occ;
+};
+template <int D, int ST>
+static const UKernel& uk() {
+  static const UKernel k = [] {
+    using C = UCfg<D, ST>;
+    auto kern = k_attn_umma<D, ST>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM);
+    return UKernel{(const void*)kern, C::SMEM, C::THREADS, occ > 0 ? occ : 1};
+  }();
+  return k;
+}
+
+static const UKernel* select_u(int D) {
+  switch (D) {
+    case 64: return &uk<64, 4>();
+    case 96: return &uk<96, 4>();
+    case 128: return &uk<128, 4>();
+  }
+  return nullptr;
+}
+
+// tcgen05 path for Qg in [umma_min_qg, 128]; TRIE_UMMA_MIN_QG overrides (0 disables)
+int attn_umma_min_qg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TRIE_UMMA_MIN_QG");
+    v = e ? atoi(e) : 33;
+  }
+  return v;
+}
+bool attn_umma_eligible(const AttnParams& p) {
+  const int Qg = p.b_live * (p.Hq / p.Hkv);
+  const int mn = attn_umma_min_qg();
+  return mn > 0 && Qg >= mn && Qg <= 128 && attn_tc_shape_ok(p);
+}
+int attn_umma_occ(const AttnParams& p) {
+  const UKernel* k = select_u(p.D);
+  return k ? k->occ : 1;
+}
+
+int launch_attn_umma(const AttnParams& p, cudaStream_t s) {
+  const UKernel* k = select_u(p.D);
+  if (!k) return trie_set_error(TRIE_EINVAL, "tcgen05 attention: unsupported head_dim %d", p.D);
+  CUtensorMap km, vm;
+  const long rows = (long)p.R * p.Hkv * p.cap;
+  int rc = cached_tensor_map(&km, p.k, p.D, rows);
+  if (!rc) rc = cached_tensor_map(&vm, p.v, p.D, rows);
+  if (rc) return rc;
+  AttnParams pp = p;
+  void* args[3] = {(void*)&km, (void*)&vm, (void*)&pp};
+  cudaLaunchKernel(k->fn, dim3(p.Hkv, p.R, p.splits), dim3(k->threads), args, (size_t)k->smem, s);
+  rc = trie_check_launch("k_attn_umma");
+  if (rc) return rc;
+  if (p.splits > 1) rc = launch_attn_combine_bf16(p, s);
+  return rc;
+}
+
+}  // namespace trie
