@@ -344,9 +344,8 @@ __global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
         tmem_wait_ld();
         if (qvalid) {
 #pragma unroll
-          for (int k = 0; k < 32; k += 4)
-            *(float4*)(pp + c + k) = make_float4(__uint_as_float(o[k]), __uint_as_float(o[k + 1]),
-                                                 __uint_as_float(o[k + 2]), __uint_as_float(o[k + 3]));
+          for (int k = 0; k < 32; k += 2)  // rows are (D + 2) floats: 8-byte aligned only
+            *(float2*)(pp + c + k) = make_float2(__uint_as_float(o[k]), __uint_as_float(o[k + 1]));
         }
       }
       if (qvalid) {
