@@ -88,7 +88,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-template <int D, int ST>
+__device__ __forceinline__ float ex2(float x) {  // MUFU.EX2; ex2(-inf) = +0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// DB: S double-buffered in TMEM (512 columns, 1 CTA/SM) or single-buffered (256 columns,
+// 2 CTAs/SM so two independent QK -> softmax -> PV chains share each SM).
+template <int D, int ST, bool DB>
 struct UCfg {
   using RG = Ring<D, ST>;
   static constexpr int STAGES = ST;
@@ -98,17 +106,17 @@ struct UCfg {
   static constexpr int NBAR = 2 * ST + 2 + 2;  // full, empty, s_full[2], p_full, pv_done
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 64 + 1024;
   static constexpr int THREADS = 6 * 32;
-  // TMEM columns: S0 [0,64), S1 [64,128), P [128,160), O [160, 160+D)
-  static constexpr int COL_S0 = 0, COL_S1 = 64, COL_P = 128, COL_O = 160;
-  static constexpr int TMEM_COLS = 512;
+  static constexpr int COL_S0 = 0, COL_S1 = DB ? 64 : 0, COL_P = DB ? 128 : 64,
+                       COL_O = DB ? 160 : 96;
+  static constexpr int TMEM_COLS = DB ? 512 : 256;
   static_assert(COL_O + D <= TMEM_COLS, "TMEM budget");
 };
 
-template <int D, int ST>
-__global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
+template <int D, int ST, bool DB>
+__global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p) {
-  using C = UCfg<D, ST>;
+  using C = UCfg<D, ST, DB>;
   using RG = typename C::RG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -154,8 +162,7 @@ __global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
     if (lane == 0) producer_loop<D, ST>(&kmap, &vmap, p, r, h, it, ring, full, empty);
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    // wait for Q in smem (softmax warps) -- named barrier 1, 160 threads
-    asm volatile("bar.sync 1, 160;");
+    asm volatile("bar.sync 1, 160;");  // Q staged by the softmax warps
     tc_fence_after();
     const uint32_t idesc_qk = umma_idesc(128, 64, 0);
     const uint32_t idesc_pv = umma_idesc(128, D, 1);
@@ -169,19 +176,17 @@ __global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
         const uint32_t d_s = tmem + ((i & 1) ? C::COL_S1 : C::COL_S0);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks) {
-          // K step ks: box ks/2 (4096 B apart for the 64-row K tile, 16 KB for the 128-row Q),
-          // +32 B inside the 64-byte swizzle row for the odd half
+          // K step ks: 32-column box ks/2 (8 KB apart for the 128-row Q, 4 KB for the 64-row
+          // K tile), + 32 B inside the 64-byte swizzled row for odd steps; SBO = 8 rows = 512 B
           const uint64_t a = umma_desc_sw64(qbase + (ks >> 1) * 128 * 64 + (ks & 1) * 32, 16, 512);
           const uint64_t b = umma_desc_sw64(kb + (ks >> 1) * TC_TR * 64 + (ks & 1) * 32, 16, 512);
           umma_ss(d_s, a, b, idesc_qk, ks > 0);
         }
-        umma_commit(&s_full[i & 1]);
+        umma_commit(&s_full[DB ? (i & 1) : 0]);
       }
       __syncwarp();
     };
-    if (ntiles > 0) issue_qk(0);
-    for (int i = 0; i < ntiles; ++i) {
-      if (i + 1 < ntiles) issue_qk(i + 1);
+    auto issue_pv = [&](int i) {
       mbar_wait(p_full, (uint32_t)i & 1u);
       tc_fence_after();
       if (lane == 0) {
@@ -189,8 +194,8 @@ __global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
         const uint32_t vb = smem_u32(ring + s * RG::STAGE_BYTES + RG::TILE_BYTES);
 #pragma unroll
         for (int kc = 0; kc < TC_TR / 16; ++kc) {
-          // V tile as MN-major B: 16 rows per K step = 2 atoms of 8 rows (1024 B); the
-          // 32-column boxes are LBO = 4096 B apart, 8-row atoms SBO = 512 B apart
+          // V tile as MN-major B: 16 rows per K step = two 8-row atoms (1024 B); the
+          // 32-column boxes are LBO = 4096 B apart, the 8-row atoms SBO = 512 B apart
           const uint64_t b = umma_desc_sw64(vb + kc * 1024, TC_TR * 64, 512);
           umma_ts(tmem + C::COL_O, tmem + C::COL_P + kc * 8, b, idesc_pv, (i > 0 || kc > 0) ? 1u : 0u);
         }
@@ -198,14 +203,25 @@ __global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
         umma_commit(pv_done);
       }
       __syncwarp();
+    };
+    if constexpr (DB) {
+      if (ntiles > 0) issue_qk(0);
+      for (int i = 0; i < ntiles; ++i) {
+        if (i + 1 < ntiles) issue_qk(i + 1);  // overlaps the softmax of tile i
+        issue_pv(i);
+      }
+    } else {
+      for (int i = 0; i < ntiles; ++i) {  // S is reused: QK(i+1) waits for softmax(i)
+        issue_qk(i);
+        issue_pv(i);
+      }
     }
   } else {
     // ===================== softmax / epilogue warps (2..5) =====================
     const int sp = warp & 3;                  // TMEM sub-partition of this warp
     const int row = sp * 32 + lane;           // query row (MMA M index)
     const int tid = threadIdx.x - 64;         // 0..127
-    // Q -> smem, 64B-swizzled K-major boxes of [128 rows][32 cols]; padding rows zero
-    {
+    {  // Q -> smem, 64B-swizzled K-major boxes of [128 rows][32 cols]; padding rows zero
       const __nv_bfloat16* q = (const __nv_bfloat16*)p.q;
       const int chunks = 128 * (D / 8);
       for (int c = tid; c < chunks; c += 128) {
@@ -221,6 +237,7 @@ __global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
       asm volatile("bar.sync 1, 160;");
     }
     const bool qvalid = row < Qg;
+    const bool warp_live = sp * 32 < Qg;      // warp-uniform: all 32 rows padding -> skip math
     const int beam = qvalid ? row / g : 0;
     const size_t mbase = (size_t)r * p.cap;
     const int lod = (p.window > 0 && qvalid) ? p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam]] - p.window + 1 : INT_MIN;
@@ -230,60 +247,71 @@ __global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
     float m_run = -INFINITY, l_run = 0.f;
     for (int i = 0; i < ntiles; ++i) {
       const int s = i % ST;
-      mbar_wait(&s_full[i & 1], (uint32_t)(i >> 1) & 1u);
+      const uint32_t spar = DB ? ((uint32_t)(i >> 1) & 1u) : ((uint32_t)i & 1u);
+      mbar_wait(&s_full[DB ? (i & 1) : 0], spar);
       mbar_wait(&full[s], (uint32_t)(i / ST) & 1u);  // (complete) makes the mask words visible
       tc_fence_after();
-      uint32_t sv[64];
-      {
-        uint32_t a[32], b[32];
-        const uint32_t col = (i & 1) ? C::COL_S1 : C::COL_S0;
-        tmem_ld32(tmem + lane_off + col, a);
-        tmem_ld32(tmem + lane_off + col + 32, b);
-        tmem_wait_ld();
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          sv[k] = a[k];
-          sv[32 + k] = b[k];
-        }
-      }
-      const int tile = it.tile0 + i;
-      const int n0 = tile * TC_TR;
-      const bool fast = tile >= it.fast_from && tile < fast_end;
-      const uint8_t* stp = ring + s * RG::STAGE_BYTES;
-      const uint32_t* tmask = (const uint32_t*)(stp + 2 * RG::TILE_BYTES);
-      const int* tdep = (const int*)(stp + 2 * RG::TILE_BYTES + TC_TR * 4);
-      float tmax = -INFINITY;
-      float x[64];
-#pragma unroll
-      for (int k = 0; k < 64; ++k) {
-        bool ok = qvalid;
-        if (!fast) {
-          const int n = n0 + k;
-          ok = ok && n < it.N && (n < it.t || ((tmask[k] >> beam) & 1u)) && tdep[k] >= lod;
-        }
-        x[k] = ok ? __uint_as_float(sv[k]) * sc : -INFINITY;
-        tmax = fmaxf(tmax, x[k]);
-      }
-      // lazy rescale: keep the running max unless the tile max exceeds it by > 8 (log2)
+      uint32_t pk[32];
       float alpha = 1.f;
       bool rescale = false;
-      if (tmax > m_run + 8.f || (m_run == -INFINITY && tmax > -INFINITY)) {
-        const float mn = tmax;
-        alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mn);
-        rescale = m_run != -INFINITY;
-        m_run = mn;
-        l_run *= alpha;
-      }
-      uint32_t pk[32];
-      float psum = 0.f;
+      if (warp_live) {
+        uint32_t a[32], bq[32];
+        const uint32_t col = (DB && (i & 1)) ? C::COL_S1 : C::COL_S0;
+        tmem_ld32(tmem + lane_off + col, a);
+        tmem_ld32(tmem + lane_off + col + 32, bq);
+        tmem_wait_ld();
+        const int tile = it.tile0 + i;
+        const int n0 = tile * TC_TR;
+        const bool fast = tile >= it.fast_from && tile < fast_end;
+        float x[64];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float p0 = x[2 * k] == -INFINITY ? 0.f : exp2f(x[2 * k] - m_run);
-        const float p1 = x[2 * k + 1] == -INFINITY ? 0.f : exp2f(x[2 * k + 1] - m_run);
-        psum += p0 + p1;
-        pk[k] = pack_bf16(p0, p1);
+        for (int k = 0; k < 32; ++k) {
+          x[k] = __uint_as_float(a[k]) * sc;
+          x[32 + k] = __uint_as_float(bq[k]) * sc;
+        }
+        if (!fast || !qvalid) {
+          const uint8_t* stp = ring + s * RG::STAGE_BYTES;
+          const uint32_t* tmask = (const uint32_t*)(stp + 2 * RG::TILE_BYTES);
+          const int* tdep = (const int*)(stp + 2 * RG::TILE_BYTES + TC_TR * 4);
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const int n = n0 + k;
+            const bool ok = qvalid && n < it.N && (n < it.t || ((tmask[k] >> beam) & 1u)) && tdep[k] >= lod;
+            x[k] = ok ? x[k] : -INFINITY;
+          }
+        }
+        float mx[8];  // tree max
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float v = x[u];
+#pragma unroll
+          for (int k = 8 + u; k < 64; k += 8) v = fmaxf(v, x[k]);
+          mx[u] = v;
+        }
+        const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        // lazy rescale: keep the running max unless the tile max exceeds it by > 8 (log2)
+        if (tmax > m_run + 8.f || (m_run == -INFINITY && tmax > -INFINITY)) {
+          alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - tmax);
+          rescale = m_run != -INFINITY;
+          m_run = tmax;
+          l_run *= alpha;
+        }
+        const float mu = m_run == -INFINITY ? 0.f : m_run;  // all masked: ex2(-inf) = 0
+        float ps[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ps[u] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float p0 = ex2(x[2 * k] - mu), p1 = ex2(x[2 * k + 1] - mu);
+          ps[k & 7] += p0 + p1;
+          pk[k] = pack_bf16(p0, p1);
+        }
+        l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) pk[k] = 0u;
       }
-      l_run += psum;
       if (i > 0) {  // PV of the previous tile must be done before P / O are touched
         mbar_wait(pv_done, (uint32_t)(i - 1) & 1u);
         tc_fence_after();
@@ -311,46 +339,48 @@ __global__ void __launch_bounds__(UCfg<D, ST>::THREADS, 1) k_attn_umma(
       tc_fence_after();
     }
     const int j = beam, ii = row % g;
-    if (p.splits == 1) {
-      __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    if (warp_live) {
+      if (p.splits == 1) {
+        __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
-      for (int c = 0; c < D; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tmem + lane_off + C::COL_O + c, o);
-        tmem_wait_ld();
-        if (qvalid) {
-          uint32_t w[16];
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_off + C::COL_O + c, o);
+          tmem_wait_ld();
+          if (qvalid) {
+            uint32_t w[16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k)
-            w[k] = pack_bf16(__uint_as_float(o[2 * k]) * inv, __uint_as_float(o[2 * k + 1]) * inv);
+            for (int k = 0; k < 16; ++k)
+              w[k] = pack_bf16(__uint_as_float(o[2 * k]) * inv, __uint_as_float(o[2 * k + 1]) * inv);
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            *(int4*)(op + c + 8 * k) = make_int4((int)w[4 * k], (int)w[4 * k + 1], (int)w[4 * k + 2], (int)w[4 * k + 3]);
+            for (int k = 0; k < 4; ++k)
+              *(int4*)(op + c + 8 * k) = make_int4((int)w[4 * k], (int)w[4 * k + 1], (int)w[4 * k + 2], (int)w[4 * k + 3]);
+          }
         }
-      }
-      if (qvalid) {
-        if (l_run == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
-        if (p.lse)
-          p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
-              l_run > 0.f ? (m_run + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
-      }
-    } else {
-      float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + row) * (D + 2);
-#pragma unroll
-      for (int c = 0; c < D; c += 32) {
-        uint32_t o[32];
-        tmem_ld32(tmem + lane_off + C::COL_O + c, o);
-        tmem_wait_ld();
         if (qvalid) {
-#pragma unroll
-          for (int k = 0; k < 32; k += 2)  // rows are (D + 2) floats: 8-byte aligned only
-            *(float2*)(pp + c + k) = make_float2(__uint_as_float(o[k]), __uint_as_float(o[k + 1]));
+          if (l_run == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
+          if (p.lse)
+            p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
+                l_run > 0.f ? (m_run + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
         }
-      }
-      if (qvalid) {
-        pp[D] = m_run;
-        pp[D + 1] = l_run;
+      } else {
+        float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + row) * (D + 2);
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_off + C::COL_O + c, o);
+          tmem_wait_ld();
+          if (qvalid) {
+#pragma unroll
+            for (int k = 0; k < 32; k += 2)  // rows are (D + 2) floats: 8-byte aligned only
+              *(float2*)(pp + c + k) = make_float2(__uint_as_float(o[k]), __uint_as_float(o[k + 1]));
+          }
+        }
+        if (qvalid) {
+          pp[D] = m_run;
+          pp[D + 1] = l_run;
+        }
       }
     }
   }
@@ -370,11 +400,11 @@ struct UKernel {
   const void* fn;
   int smem, threads, occ;
 };
-template <int D, int ST>
+template <int D, int ST, bool DB>
 static const UKernel& uk() {
   static const UKernel k = [] {
-    using C = UCfg<D, ST>;
-    auto kern = k_attn_umma<D, ST>;
+    using C = UCfg<D, ST, DB>;
+    auto kern = k_attn_umma<D, ST, DB>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int occ = 0;
@@ -384,11 +414,26 @@ static const UKernel& uk() {
   return k;
 }
 
+// TRIE_UMMA_DB=1: double-buffered S, 4 stages, 1 CTA/SM; default 0: single S, 2 stages,
+// 2 CTAs/SM
+static int umma_db() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TRIE_UMMA_DB");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+template <int D>
+static const UKernel& select_ud() {
+  if (umma_db()) return uk<D, 4, true>();
+  return uk<D, 2, false>();
+}
 static const UKernel* select_u(int D) {
   switch (D) {
-    case 64: return &uk<64, 4>();
-    case 96: return &uk<96, 4>();
-    case 128: return &uk<128, 4>();
+    case 64: return &select_ud<64>();
+    case 96: return &select_ud<96>();
+    case 128: return &select_ud<128>();
   }
   return nullptr;
 }
