@@ -264,12 +264,13 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
         const int n0 = tile * TC_TR;
         const bool fast = tile >= it.fast_from && tile < fast_end;
         float x[64];
+        const float scq = qvalid ? sc : 0.f;  // padding rows: every score -> -inf below
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-          x[k] = __uint_as_float(a[k]) * sc;
-          x[32 + k] = __uint_as_float(bq[k]) * sc;
+          x[k] = qvalid ? __uint_as_float(a[k]) * scq : -INFINITY;
+          x[32 + k] = qvalid ? __uint_as_float(bq[k]) * scq : -INFINITY;
         }
-        if (!fast || !qvalid) {
+        if (!fast) {  // warp-uniform
           const uint8_t* stp = ring + s * RG::STAGE_BYTES;
           const uint32_t* tmask = (const uint32_t*)(stp + 2 * RG::TILE_BYTES);
           const int* tdep = (const int*)(stp + 2 * RG::TILE_BYTES + TC_TR * 4);
@@ -414,13 +415,13 @@ static const UKernel& uk() {
   return k;
 }
 
-// TRIE_UMMA_DB=1: double-buffered S, 4 stages, 1 CTA/SM; default 0: single S, 2 stages,
+// TRIE_UMMA_DB=1 (default): double-buffered S, 4 stages, 1 CTA/SM; 0: single S, 2 stages,
 // 2 CTAs/SM
 static int umma_db() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("TRIE_UMMA_DB");
-    v = e ? atoi(e) : 0;
+    v = e ? atoi(e) : 1;  // r05 sweep R=16: DB=1 4.12 TB/s (b=16) vs DB=0 2.85
   }
   return v;
 }
