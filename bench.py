@@ -45,7 +45,7 @@ WORKLOADS = {
                           D=128, V=131072, t=4096, b=4, s=128, R=16, W=4096, theta=1e8),
     # configs[4] kernel-level sweep point (b set by --beam)
     "sweep": dict(name="llama3.1-8b-gqa-t8192-sweep", L=4, Hq=32, Hkv=8, D=128, V=128256, t=8192,
-                  b=16, s=128, R=4, W=0, theta=500000.0),
+                  b=16, s=128, R=16, W=0, theta=500000.0),  # SURVEY cfg5: R in {1, 4, 16}
 }
 
 
