@@ -150,6 +150,10 @@ class HotPath:
         self.graphs = {}
         self.launches_per_graph = {}
         self.k = 0  # steps done in the current job
+        from paper_2502_00085_b200 import _lib
+        self.plan = {var: _lib.trie_attn_plan_info(self.st.cfg, bl, self.rows_hint)
+                     for var, bl in (("first", 1), ("steady", b))}
+        self.fused = {var: self.plan[var]["fused_rope"] for var in self.plan}
 
     def step_ops(self, var, slot, events=None):
         """Enqueue one step (all §8(a) rows) on the current stream."""
@@ -157,14 +161,23 @@ class HotPath:
         d = self.inp[(var, slot)]
         if var == "first":
             st.reset()
+        fused = self.fused[var]
+        if events is not None and fused:  # the layer loop is L attention launches only
+            events[0][0].record()
         for l in range(L):
             q, k, v = d["views"][l]
+            if fused:  # a-1 + a-3 in one launch
+                st.attn_decode_rope(q, k, v, self.kp[l], self.vp[l], self.wl["theta"], d["out"],
+                                    rows_hint=self.rows_hint)
+                continue
             st.rope_kv_append(q, k, v, self.kp[l], self.vp[l], self.wl["theta"])
             if events is not None:
                 events[l][0].record()
             st.attn_decode(q, self.kp[l], self.vp[l], d["out"], rows_hint=self.rows_hint)
             if events is not None:
                 events[l][1].record()
+        if events is not None and fused:
+            events[0][1].record()
         st.beam_step(d["logits"], self.sel_p, self.sel_t, self.sel_s)
         st.prune_compact(self.kp, self.vp)
 
@@ -178,8 +191,9 @@ class HotPath:
                 for timed in (False, True):
                     evs = None
                     if timed:
+                        n_pairs = 1 if self.fused[var] else self.L
                         evs = [(torch.cuda.Event(enable_timing=True, external=True),
-                                torch.cuda.Event(enable_timing=True, external=True)) for _ in range(self.L)]
+                                torch.cuda.Event(enable_timing=True, external=True)) for _ in range(n_pairs)]
                     g = torch.cuda.CUDAGraph()
                     n0 = _lib.trie_launch_count()
                     with torch.cuda.graph(g):
@@ -277,9 +291,13 @@ def run_gpu(args):
     def harvest(slot):
         var_p, kj_p, i_p = pending.pop(slot)
         end_ev[slot].synchronize()  # only step i_p; step i_p + 1 keeps the GPU busy
-        for e0, e1 in hp.ev[(var_p, slot)]:
-            attn_ms.append(e0.elapsed_time(e1))
-            attn_step.append((i_p, kj_p))
+        evs = hp.ev[(var_p, slot)]
+        per = hp.L // len(evs)  # fused: one pair spans the L attention launches of the step
+        for e0, e1 in evs:
+            dt = e0.elapsed_time(e1)
+            for _ in range(per):
+                attn_ms.append(dt / per)
+                attn_step.append((i_p, kj_p))
 
     # Region A (value): plain step graphs back to back.
     t0.record(stream)
@@ -335,6 +353,7 @@ def run_gpu(args):
                            new_tokens=s, layers=L, q_heads=hp.Hq, kv_heads=hp.Hkv, head_dim=hp.D,
                            vocab=hp.V, window=hp.W, gc_interval=1, parallelism=f"request-dp{world}",
                            execution="cuda-graph replay per step",
+                           attention={k: v for k, v in hp.plan["steady"].items()},
                            l2=(f"no flush: each layer's pool is re-read once per step and the per-step "
                                f"KV footprint ({kv_fp / 1e6:.0f} MB) > L2 (126 MB)")))
     res["roofline"] = dict(kernel="trie_attn_decode", bound="hbm", achieved=round(ach, 1), peak=peak,

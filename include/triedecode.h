@@ -153,6 +153,29 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
                      float* lse, void* scratch, size_t scratch_bytes, cudaStream_t stream);
 
 /*
+ * Which attention kernel a configuration uses (host only): info_host[0] = path (0 CUDA-core
+ * fp32/other, 1 narrow mma.sync, 2 wide mma.sync, 3 tcgen05/TMEM, 4 persistent),
+ * [1] = split-K count, [2] = 1 if trie_attn_decode_rope fuses into one launch, [3] = Qg.
+ */
+int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,
+                        int32_t* info_host);
+
+/*
+ * a-1 + a-3 fused (one launch when the narrow tensor-core kernel applies: bf16, D in
+ * {64, 96, 128}, b_live * Hq/Hkv <= 16): the same result as trie_rope_kv_append followed
+ * by trie_attn_decode over the handle's trie (window = cfg.window), except that q and
+ * k_new are read un-rotated and not written back.  Each attention CTA rotates its own
+ * query heads at the beams' depths and, if its tiles contain leaf slots, rotates and
+ * appends those leaves' K/V rows (write-before-read, §3.4 / Alg. 3 l.7) before loading
+ * the tile.  Other shapes run the two steps as two launches (q, k_new then hold their
+ * rotated values).  Arguments as in the two calls; scratch >= trie_attn_scratch_bytes.
+ */
+int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, const void* v_new,
+                          void* k_pool, void* v_pool, float rope_theta, int32_t rows_hint,
+                          void* out, float* lse, void* scratch, size_t scratch_bytes,
+                          cudaStream_t stream);
+
+/*
  * a-4 + a-5 (+ a-2 update): one beam step (Alg. 2 l.9-11; Alg. 1 l.6 P:116).
  * logits [R][b_live][V] fp32 (b_live = 1 on the first call).  Per request:
  *   lp_j[v] = x_j[v] - lse_j,  lse_j = max + log sum exp(x_j - max);

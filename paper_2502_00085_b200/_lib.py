@@ -21,7 +21,7 @@ TRIE_ST_CAPACITY, TRIE_ST_PARENT, TRIE_ST_EMPTY_ROW, TRIE_ST_LEAF = 1, 2, 4, 8
 SYMBOLS = ["trie_workspace_bytes", "trie_create", "trie_reset", "trie_destroy", "trie_get_arrays",
            "trie_rope_kv_append", "trie_attn_scratch_bytes", "trie_attn_decode", "trie_beam_step",
            "trie_append", "trie_prune_compact", "trie_read_hyps", "trie_status", "trie_last_error",
-           "trie_version", "trie_launch_count"]
+           "trie_version", "trie_launch_count", "trie_attn_decode_rope", "trie_attn_plan_info"]
 
 
 class trie_cfg(ctypes.Structure):
@@ -60,6 +60,8 @@ def load(path: str = LIB_PATH):
         "trie_attn_scratch_bytes": (SZ, [CP, I32, I32]),
         "trie_attn_decode": (ctypes.c_int, [CP, I32, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P,
                                             SZ, P]),
+        "trie_attn_decode_rope": (ctypes.c_int, [P, P, P, P, P, P, ctypes.c_float, I32, P, P, P, SZ, P]),
+        "trie_attn_plan_info": (ctypes.c_int, [CP, I32, I32, P]),
         "trie_beam_step": (ctypes.c_int, [P, P, P, P, P, P]),
         "trie_append": (ctypes.c_int, [P, P, P, P, P]),
         "trie_prune_compact": (ctypes.c_int, [P, P, P, P]),
@@ -153,6 +155,14 @@ def trie_attn_decode(cfg, b_live, q, k_pool, v_pool, prompt_len, parent, depth, 
                                    _ptr(lse), _ptr(scratch), sb, _stream(stream)), "trie_attn_decode")
 
 
+def trie_attn_decode_rope(h, q, k_new, v_new, k_pool, v_pool, rope_theta, rows_hint, out, lse, scratch,
+                          stream=None):
+    sb = 0 if scratch is None else scratch.numel() * scratch.element_size()
+    _check(load().trie_attn_decode_rope(h, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(k_pool), _ptr(v_pool),
+                                        float(rope_theta), rows_hint, _ptr(out), _ptr(lse), _ptr(scratch), sb,
+                                        _stream(stream)), "trie_attn_decode_rope")
+
+
 def trie_beam_step(h, logits, sel_parent_beam=None, sel_token=None, new_score=None, stream=None):
     _check(load().trie_beam_step(h, _ptr(logits), _ptr(sel_parent_beam), _ptr(sel_token),
                                  _ptr(new_score), _stream(stream)), "trie_beam_step")
@@ -198,3 +208,13 @@ def trie_last_error() -> str:
 
 def trie_launch_count() -> int:
     return int(load().trie_launch_count())
+
+
+ATTN_PATHS = {0: "cuda-core", 1: "narrow-mma.sync", 2: "wide-mma.sync", 3: "tcgen05-tmem", 4: "persistent"}
+
+
+def trie_attn_plan_info(cfg: trie_cfg, b_live: int, rows_hint: int = 0) -> dict:
+    info = (ctypes.c_int32 * 4)()
+    _check(load().trie_attn_plan_info(ctypes.byref(cfg), b_live, rows_hint, ctypes.cast(info, ctypes.c_void_p)),
+           "trie_attn_plan_info")
+    return dict(path=ATTN_PATHS.get(info[0], str(info[0])), splits=info[1], fused_rope=bool(info[2]), Qg=info[3])

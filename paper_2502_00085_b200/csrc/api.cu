@@ -246,10 +246,11 @@ struct AttnPlan {
   size_t counter_bytes, part_bytes, mask_bytes;
 };
 
-static AttnPlan attn_plan(const trie_cfg* c, int b_live, int rows_hint) {
+static AttnPlan attn_plan(const trie_cfg* c, int b_live, int rows_hint, bool rope = false) {
   AttnPlan pl{};
   const int rows = rows_hint > 0 ? rows_hint : c->capacity;
-  const trie::AttnParams sp = shape_params(c, b_live);
+  trie::AttnParams sp = shape_params(c, b_live);
+  sp.rope = rope ? 1 : 0;
   pl.persist = trie::attn_persist_enabled() && trie::attn_tc_shape_ok(sp);
   if (pl.persist) {
     pl.splits = trie::attn_persist_splits(sp, rows, sm_count());
@@ -311,6 +312,75 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
   if (trie::attn_tc_supported(p))
     return pl.persist ? trie::launch_attn_persist(p, stream) : trie::launch_attn_tc(p, stream);
   return trie::launch_attn_v1(p, stream);
+}
+
+int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,
+                        int32_t* info_host) {
+  int rc = validate(cfg);
+  if (rc) return rc;
+  if (!info_host || b_live < 1 || b_live > cfg->beam_width)
+    return trie_set_error(TRIE_EINVAL, "bad argument");
+  trie::AttnParams p = shape_params(cfg, b_live);
+  const AttnPlan pl = attn_plan(cfg, b_live, rows_hint);
+  const int Qg = b_live * (cfg->n_q_heads / cfg->n_kv_heads);
+  int path = 0;
+  if (trie::attn_tc_shape_ok(p))
+    path = pl.persist ? 4 : trie::attn_umma_eligible(p) ? 3 : (Qg <= 16 ? 1 : 2);
+  p.k = p.v = (const void*)(uintptr_t)256;  // aligned placeholders for the shape test
+  const bool fused = !pl.persist && trie::attn_rope_fusable(p);
+  info_host[0] = path;
+  info_host[1] = fused ? attn_plan(cfg, b_live, rows_hint, true).splits : pl.splits;
+  info_host[2] = fused ? 1 : 0;
+  info_host[3] = Qg;
+  return TRIE_OK;
+}
+
+// ---- fused a-1 + a-3 -------------------------------------------------------------------
+int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, const void* v_new,
+                          void* k_pool, void* v_pool, float rope_theta, int32_t rows_hint,
+                          void* out, float* lse, void* scratch, size_t scratch_bytes,
+                          cudaStream_t stream) {
+  if (!h || !q || !k_new || !v_new || !k_pool || !v_pool || !out)
+    return trie_set_error(TRIE_EINVAL, "null argument");
+  if (!(rope_theta > 1.f)) return trie_set_error(TRIE_EINVAL, "rope_theta must be > 1");
+  const trie_cfg* cfg = &h->cfg;
+  const int b_live = h->b_live;
+  trie::AttnParams p = shape_params(cfg, b_live);
+  p.q = q;
+  p.k = k_pool;
+  p.v = v_pool;
+  p.out = out;
+  p.lse = lse;
+  p.tlen = h->tlen;
+  p.depth = h->depth;
+  p.leaf = h->leaf;
+  p.nn = h->n_nodes;
+  p.mask = h->mask;
+  p.status = h->status;
+  p.window = cfg->window;
+  p.rope = 1;
+  p.k_new = k_new;
+  p.v_new = v_new;
+  for (int i = 0; i < cfg->head_dim / 2; ++i)
+    p.inv_freq[i] = pow((double)rope_theta, -2.0 * i / (double)cfg->head_dim);
+  const bool fuse = !trie::attn_persist_enabled() && trie::attn_rope_fusable(p) &&
+                    (((uintptr_t)q | (uintptr_t)k_new | (uintptr_t)v_new) & 3) == 0;
+  if (!fuse) {  // two launches: rotate + append, then attention over the handle's trie
+    int rc = trie::launch_rope_append(h, const_cast<void*>(q), const_cast<void*>(k_new), v_new,
+                                      k_pool, v_pool, rope_theta, stream);
+    if (rc) return rc;
+    return trie_attn_decode(cfg, b_live, q, k_pool, v_pool, h->tlen, h->parent, h->depth, h->leaf,
+                            h->n_nodes, h->mask, cfg->window, rows_hint, out, lse, scratch,
+                            scratch_bytes, stream);
+  }
+  const AttnPlan pl = attn_plan(cfg, b_live, rows_hint, true);
+  const size_t need = pl.counter_bytes + pl.part_bytes;
+  if (need > 0 && (!scratch || scratch_bytes < need))
+    return trie_set_error(TRIE_ECAPACITY, "attention scratch %zu < %zu", scratch_bytes, need);
+  p.aux = scratch;
+  p.part = (float*)((char*)scratch + pl.counter_bytes);
+  p.splits = pl.splits;
+  return trie::launch_attn_tc(p, stream);
 }
 
 // ---- beam step / append / prune --------------------------------------------------------

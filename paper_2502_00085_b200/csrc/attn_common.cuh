@@ -21,10 +21,17 @@ struct AttnParams {
   int R, b_live, Hq, Hkv, D, cap, window, splits;
   float scale_log2;       // log2(e) / sqrt(D)
   int bf16;
+  // fused RoPE + KV append (trie_attn_decode_rope): q is read un-rotated, the leaves'
+  // k_new/v_new rows are rotated/appended into the pools by the CTA owning their tile
+  int rope;
+  const void* k_new;      // [R][b_live][Hkv][D]
+  const void* v_new;      // [R][b_live][Hkv][D]
+  double inv_freq[128];   // theta^(-2i/D), i < D/2 (host-computed in fp64)
 };
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);
 int launch_attn_tc(const AttnParams& p, cudaStream_t s);
+bool attn_rope_fusable(const AttnParams& p);
 bool attn_tc_supported(const AttnParams& p);
 int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s);
 int attn_plan_splits(const AttnParams& p, int rows_est, int sms);

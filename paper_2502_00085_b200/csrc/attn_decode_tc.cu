@@ -37,7 +37,7 @@ namespace trie {
 // =========================================================================================
 // narrow: Qg <= 8 * NQ (NQ in {1, 2}); CTA = producer warp + one consumer warp
 // =========================================================================================
-template <int D, int NQ, int ST>
+template <int D, int NQ, int ST, bool ROPE = false>
 struct NarrowCfg {
   static constexpr int STAGES = ST;
   using RG = Ring<D, STAGES>;
@@ -45,22 +45,28 @@ struct NarrowCfg {
   static constexpr int DM = D / 16;     // m-tiles of O^T (over D)
   // epilogue staging [8*NQ][D+4] floats aliases the ring (all tiles consumed by then)
   static_assert(NQ * 8 * (D + 4) * 4 <= RG::RING_BYTES, "staging must fit in the ring");
-  static constexpr int SMEM = RG::RING_BYTES + 2 * STAGES * 8 + 64 + 1024;
+  static constexpr int OFF_BAR = RG::RING_BYTES;
+  static constexpr int OFF_TAB = OFF_BAR + 128;  // fused RoPE: (cos, sin)[beam][D/2]
+  static constexpr int TAB = ROPE ? NQ * 8 * (D / 2) * 8 : 0;
+  static constexpr int SMEM = OFF_TAB + TAB + 1024;
+  static_assert(2 * ST * 8 + 8 + (int)sizeof(ItemInfo) <= 128, "barrier area");
 };
 
-template <int D, int NQ, int ST>
+template <int D, int NQ, int ST, bool ROPE = false>
 __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUtensorMap kmap,
                                                     const __grid_constant__ CUtensorMap vmap,
                                                     const AttnParams p) {
-  using C = NarrowCfg<D, NQ, ST>;
+  using C = NarrowCfg<D, NQ, ST, ROPE>;
   using RG = typename C::RG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ring = smem;
   float* stage_out = (float*)smem;  // epilogue only
-  uint64_t* full = (uint64_t*)(smem + RG::RING_BYTES);
+  uint64_t* full = (uint64_t*)(smem + C::OFF_BAR);
   uint64_t* empty = full + C::STAGES;
-  ItemInfo* info = (ItemInfo*)(empty + C::STAGES);
+  uint64_t* app_done = empty + C::STAGES;
+  ItemInfo* info = (ItemInfo*)(app_done + 1);
+  float2* cs_tab = (float2*)(smem + C::OFF_TAB);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -69,19 +75,67 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    mbar_init(app_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     item_setup(p, r, split, info);
   }
   __syncthreads();
   const ItemInfo it = *info;
   if (warp == 0) {
-    if (lane == 0) producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+    if (lane == 0) {
+      if constexpr (ROPE)
+        producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
+                                    it.N - p.b_live);
+      else
+        producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+    }
     return;
   }
   // ===== consumer warp =====
   const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
   const int gq = lane >> 2, cq = lane & 3;
   const size_t mbase = (size_t)r * p.cap;
+  constexpr int HALF = D / 2;
+  if constexpr (ROPE) {
+    // (a) one angle per (beam, frequency): pos * theta^(-2i/D) in fp64, reduced mod 2*pi
+    //     in fp64, then fp32 sincos (reading R16; same positions as trie_rope_kv_append)
+    for (int e = lane; e < p.b_live * HALF; e += 32) {
+      const int j = e / HALF, i = e % HALF;
+      const double ang = (double)p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + j]] * p.inv_freq[i];
+      const double red = ang - rint(ang * 0.15915494309189535) * 6.283185307179586;
+      float sn, cs;
+      sincosf((float)red, &sn, &cs);
+      cs_tab[e] = make_float2(cs, sn);
+    }
+    __syncwarp();
+    // (b) write-before-read append of the leaves whose slots lie in this CTA's tiles
+    const int slot_lo = it.tile0 * TC_TR, slot_hi = (it.tile0 + it.ntiles) * TC_TR;
+    const __nv_bfloat16* kn = (const __nv_bfloat16*)p.k_new;
+    const __nv_bfloat16* vn = (const __nv_bfloat16*)p.v_new;
+    __nv_bfloat16* kpool = (__nv_bfloat16*)p.k;
+    __nv_bfloat16* vpool = (__nv_bfloat16*)p.v;
+    for (int e = lane; e < p.b_live * HALF; e += 32) {
+      const int j = e / HALF, i = e % HALF;
+      const int slot = p.leaf[r * TRIE_MAX_BEAMS + j];
+      if (slot < slot_lo || slot >= slot_hi) continue;
+      const __nv_bfloat16* src = kn + (((size_t)r * p.b_live + j) * p.Hkv + h) * D;
+      const float x1 = __bfloat162float(src[i]), x2 = __bfloat162float(src[i + HALF]);
+      const float2 c = cs_tab[e];
+      __nv_bfloat16* dst = kpool + (((size_t)r * p.Hkv + h) * p.cap + slot) * D;
+      dst[i] = __float2bfloat16_rn(x1 * c.x - x2 * c.y);
+      dst[i + HALF] = __float2bfloat16_rn(x2 * c.x + x1 * c.y);
+    }
+    for (int e = lane; e < p.b_live * D; e += 32) {
+      const int j = e / D, d = e % D;
+      const int slot = p.leaf[r * TRIE_MAX_BEAMS + j];
+      if (slot < slot_lo || slot >= slot_hi) continue;
+      vpool[(((size_t)r * p.Hkv + h) * p.cap + slot) * D + d] =
+          vn[(((size_t)r * p.b_live + j) * p.Hkv + h) * D + d];
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+    __syncwarp();
+    if (lane == 0) mbar_arrive(app_done);
+  }
   // queries held by this thread in the S^T / O^T fragments: columns 2cq, 2cq+1 of each n-tile
   int beam[NQ][2], lod[NQ][2];
   bool qok[NQ][2];
@@ -107,8 +161,24 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       if (m < Qg) src = q + (((size_t)r * p.b_live + m / g) * p.Hq + h * g + m % g) * D;
 #pragma unroll
       for (int ks = 0; ks < C::KS; ++ks) {
-        qb[nq][ks][0] = src ? *(const uint32_t*)(src + ks * 16 + cq * 2) : 0u;
-        qb[nq][ks][1] = src ? *(const uint32_t*)(src + ks * 16 + 8 + cq * 2) : 0u;
+#pragma unroll
+        for (int hi = 0; hi < 2; ++hi) {
+          const int d = ks * 16 + hi * 8 + cq * 2;
+          uint32_t v = src ? *(const uint32_t*)(src + d) : 0u;
+          if constexpr (ROPE) {
+            if (src) {  // rotate-half at the beam's depth, rounded to bf16 like trie_rope_kv_append
+              const int pd = d < HALF ? d + HALF : d - HALF;
+              const uint32_t pv = *(const uint32_t*)(src + pd);
+              const float2 x = __bfloat1622float2(*(const __nv_bfloat162*)&v);
+              const float2 xp = __bfloat1622float2(*(const __nv_bfloat162*)&pv);
+              const int i0 = d % HALF, j = m / g;
+              const float2 c0 = cs_tab[j * HALF + i0], c1 = cs_tab[j * HALF + i0 + 1];
+              const float sg = d < HALF ? -1.f : 1.f;
+              v = pack_bf16(x.x * c0.x + sg * xp.x * c0.y, x.y * c1.x + sg * xp.y * c1.y);
+            }
+          }
+          qb[nq][ks][hi] = v;
+        }
       }
     }
   }
@@ -643,9 +713,10 @@ static TcKernel make_tc(Kern kern, int smem, int threads) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   return TcKernel{(const void*)kern, smem, threads, occ > 0 ? occ : 1};
 }
-template <int D, int NQ, int ST>
+template <int D, int NQ, int ST, bool ROPE = false>
 static const TcKernel& narrow_k() {
-  static const TcKernel k = make_tc(k_attn_narrow<D, NQ, ST>, NarrowCfg<D, NQ, ST>::SMEM, 64);
+  static const TcKernel k =
+      make_tc(k_attn_narrow<D, NQ, ST, ROPE>, NarrowCfg<D, NQ, ST, ROPE>::SMEM, 64);
   return k;
 }
 template <int D, int MT, int RS>
@@ -687,29 +758,35 @@ static int narrow_stages() {
   }
   return v;
 }
-template <int D, int NQ>
+template <int D, int NQ, bool ROPE>
 static const TcKernel& narrow_sel() {
   switch (narrow_stages()) {
-    case 3: return narrow_k<D, NQ, 3>();
-    case 4: return narrow_k<D, NQ, 4>();
-    default: return narrow_k<D, NQ, 2>();
+    case 3: return narrow_k<D, NQ, 3, ROPE>();
+    case 4: return narrow_k<D, NQ, 4, ROPE>();
+    default: return narrow_k<D, NQ, 2, ROPE>();
   }
 }
 template <int D>
-static const TcKernel& select_d(int Qg) {
-  if (Qg <= 8) return narrow_sel<D, 1>();
-  if (Qg <= 16) return narrow_sel<D, 2>();
+static const TcKernel& select_d(int Qg, bool rope) {
+  if (Qg <= 8) return rope ? narrow_sel<D, 1, true>() : narrow_sel<D, 1, false>();
+  if (Qg <= 16) return rope ? narrow_sel<D, 2, true>() : narrow_sel<D, 2, false>();
   if (Qg <= 32) return wide_sel<D, 2>();
   if (Qg <= 64) return wide_sel<D, 4>();
   return wide_sel<D, 8>();
 }
-static const TcKernel* select_tc(int D, int Qg) {
+static const TcKernel* select_tc(int D, int Qg, bool rope = false) {
   switch (D) {
-    case 64: return &select_d<64>(Qg);
-    case 96: return &select_d<96>(Qg);
-    case 128: return &select_d<128>(Qg);
+    case 64: return &select_d<64>(Qg, rope);
+    case 96: return &select_d<96>(Qg, rope);
+    case 128: return &select_d<128>(Qg, rope);
   }
   return nullptr;
+}
+
+// The fused RoPE + append variant exists for the narrow kernel (Qg <= 16).
+bool attn_rope_fusable(const AttnParams& p) {
+  const int Qg = p.b_live * (p.Hq / p.Hkv);
+  return attn_tc_supported(p) && !attn_umma_eligible(p) && Qg <= 16;
 }
 
 bool attn_tc_shape_ok(const AttnParams& p) {
@@ -732,7 +809,7 @@ int attn_plan_splits(const AttnParams& p, int rows_est, int sms) {
   if (attn_umma_eligible(p)) {
     occ = attn_umma_occ(p);
   } else if (attn_tc_shape_ok(p)) {
-    const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv));
+    const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv), p.rope != 0);
     if (k) occ = k->occ;
   }
   const int slots = occ * sms;
@@ -746,7 +823,7 @@ int attn_plan_splits(const AttnParams& p, int rows_est, int sms) {
 
 int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
   if (attn_umma_eligible(p)) return launch_attn_umma(p, s);
-  const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv));
+  const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv), p.rope != 0);
   if (!k) return trie_set_error(TRIE_EINVAL, "tensor-core attention: unsupported head_dim %d", p.D);
   CUtensorMap km, vm;
   const long rows = (long)p.R * p.Hkv * p.cap;

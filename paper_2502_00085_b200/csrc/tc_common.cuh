@@ -145,14 +145,22 @@ template <int D, int STAGES>
 __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUtensorMap* vmap,
                                               const AttnParams& p, int r, int h,
                                               const ItemInfo& it, uint8_t* ring, uint64_t* full,
-                                              uint64_t* empty) {
+                                              uint64_t* empty, uint64_t* app_done = nullptr,
+                                              int first_leaf_slot = INT_MAX) {
   using RG = Ring<D, STAGES>;
   const int row_base = (r * p.Hkv + h) * p.cap;
   const size_t mbase = (size_t)r * p.cap;
+  bool appended = app_done == nullptr;
   for (int i = 0; i < it.ntiles; ++i) {
     const int s = i % STAGES;
     const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
     mbar_wait(&empty[s], ph ^ 1u);
+    if (!appended && (it.tile0 + i + 1) * TC_TR > first_leaf_slot) {
+      // fused RoPE: the consumer wrote this tile's leaf K/V rows (generic proxy) and
+      // fenced them for the async proxy before arriving; TMA may read them now
+      mbar_wait(app_done, 0u);
+      appended = true;
+    }
     const uint32_t st = smem_u32(ring + s * RG::STAGE_BYTES);
     const int n0 = (it.tile0 + i) * TC_TR;
     // mask / depth words clamped to the [R][cap] arrays (cap % 4 == 0: 16-byte granules)

@@ -84,6 +84,15 @@ class TrieState:
                            self.depth, self.leaf, self.n_nodes, self.beam_mask if use_mask else None,
                            self.window, rows_hint, out, lse, self.attn_scratch, stream)
 
+    def attn_decode_rope(self, q, k_new, v_new, k_pool_l, v_pool_l, rope_theta, out, lse=None,
+                         rows_hint=0, stream=None):
+        """Fused a-1 + a-3: RoPE at depth + KV append + trie attention in one launch."""
+        need = L.trie_attn_scratch_bytes(self.cfg, self.b_live, rows_hint)
+        if self.attn_scratch is None or self.attn_scratch.numel() < need:
+            self.attn_scratch = torch.zeros(need, dtype=torch.uint8, device=self.device)
+        L.trie_attn_decode_rope(self.h, q, k_new, v_new, k_pool_l, v_pool_l, rope_theta, rows_hint, out,
+                                lse, self.attn_scratch, stream)
+
     def beam_step(self, logits, sel_parent=None, sel_token=None, new_score=None, stream=None):
         L.trie_beam_step(self.h, logits, sel_parent, sel_token, new_score, stream)
 

@@ -108,3 +108,61 @@ def test_rope_kv_append_matches_oracle(dt):
             assert rel_err(q[r, j].float().cpu().numpy(), qr) <= tol
             assert rel_err(kp[0, r, :, leaf[r, j]].float().cpu().numpy(), kr) <= tol
             assert np.array_equal(vp[0, r, :, leaf[r, j]].float().cpu().numpy(), v0[r, j])
+
+
+@pytest.mark.parametrize("name,R,b,t_max,Hq,Hkv,D,W", [
+    ("phi-fused", 2, 4, 300, 8, 8, 96, 0),
+    ("gqa-fused", 2, 4, 200, 8, 2, 128, 0),
+    ("swa-fused", 1, 4, 150, 4, 1, 64, 40),
+    ("split-fused", 1, 2, 1500, 2, 2, 128, 0),
+    ("wide-unfused", 1, 8, 130, 8, 2, 128, 0),   # Qg = 32: two-launch fallback
+])
+def test_fused_rope_attention_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W):
+    """trie_attn_decode_rope == RoPE at depth (§3.4) + write-before-read append + trie
+    attention, vs the oracle (rope_rotate_half + attn_ref on its own trie)."""
+    need_gpu()
+    from paper_2502_00085_b200.trie import TrieState
+    seed = zlib.crc32(name.encode()) % 1000
+    V, steps, base = 300, 6, 500000.0
+    prompts, lens = synth.prompts(seed, R, t_max, V)
+    sels = per_request_selections(seed, R, steps, b, V, 0.5)
+    cap = (t_max + b * steps + b + 63) // 64 * 64
+    st = TrieState(R, b, t_max, cap, 1, Hq, Hkv, D, V, prompts, lens, window=W, dtype=torch.bfloat16)
+    kp, vp = st.new_pools()
+    for par, tok in sels:
+        st.append(torch.as_tensor(par, device="cuda"), torch.as_tensor(tok, device="cuda"))
+        st.prune_compact(kp, vp)
+    tries = build_tries(prompts, lens, sels, b, g=1, final_gc=True)
+    K = synth.normal(seed, 1, (R, Hkv, cap, D))
+    Vv = synth.normal(seed, 2, (R, Hkv, cap, D))
+    tK = torch.as_tensor(K, dtype=torch.float32).to(torch.bfloat16).cuda()
+    tV = torch.as_tensor(Vv, dtype=torch.float32).to(torch.bfloat16).cuda()
+    kp[0].copy_(tK)
+    vp[0].copy_(tV)
+    q = torch.as_tensor(synth.normal(seed, 3, (R, b, Hq, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
+    kn = torch.as_tensor(synth.normal(seed, 4, (R, b, Hkv, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
+    vn = torch.as_tensor(synth.normal(seed, 5, (R, b, Hkv, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
+    q0, k0, v0 = (x.float().cpu().numpy().astype(np.float64) for x in (q, kn, vn))
+    Kh, Vh = tK.float().cpu().numpy().astype(np.float64), tV.float().cpu().numpy().astype(np.float64)
+    out = torch.empty_like(q)
+    lse = torch.empty(R, b, Hq, dtype=torch.float32, device="cuda")
+    st.attn_decode_rope(q, kn, vn, kp[0], vp[0], base, out, lse, rows_hint=t_max + steps)
+    torch.cuda.synchronize()
+    assert st.status() == 0
+    o, l = out.float().cpu().numpy(), lse.cpu().numpy()
+    kpool_after = kp[0].float().cpu().numpy()
+    vpool_after = vp[0].float().cpu().numpy()
+    for r in range(R):
+        T = tries[r]
+        Kr, Vr = Kh[r].copy(), Vh[r].copy()
+        qr = np.zeros((b, Hq, D))
+        for j, leaf in enumerate(T.leaves):
+            pos = T.depth[leaf]
+            qr[j] = rope_rotate_half(q0[r, j], pos, base)
+            Kr[:, leaf] = rope_rotate_half(k0[r, j], pos, base)
+            Vr[:, leaf] = v0[r, j]
+            assert rel_err(kpool_after[r, :, leaf], Kr[:, leaf]) <= 1e-2   # appended, rotated
+            assert np.array_equal(vpool_after[r, :, leaf], Vr[:, leaf])
+        o_ref, lse_ref = attn_ref(qr, Kr[:, :T.N], Vr[:, :T.N], T, window=W)
+        assert rel_err(o[r], o_ref) <= 2e-2, f"{name} r={r}: {rel_err(o[r], o_ref)}"
+        assert np.abs(l[r] - lse_ref).max() <= 2e-2 * max(1.0, np.abs(lse_ref).max())
