@@ -82,6 +82,7 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
   char* sp = take(R * b * 4);
   char* st = take(R * b * 4);
   char* ss = take(R * b * 4);
+  char* rtab = take(R * TRIE_MAX_BEAMS * (c->head_dim / 2) * 8);
   if (h) {
     h->token = (int32_t*)token;
     h->parent = (int32_t*)parent;
@@ -103,6 +104,7 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
     h->sel_parent = (int32_t*)sp;
     h->sel_token = (int32_t*)st;
     h->sel_score = (float*)ss;
+    h->rope_tab = (float2*)rtab;
     h->chunks = (int32_t)chunks;
   }
   return off;
@@ -174,6 +176,7 @@ int trie_reset(trie_handle* h, cudaStream_t stream) {
   if (!h) return trie_set_error(TRIE_EINVAL, "null handle");
   h->b_live = 1;
   h->steps = 0;
+  h->rope_tab_steps = -1;
   return trie::launch_init(h, stream);
 }
 
@@ -361,8 +364,7 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.rope = 1;
   p.k_new = k_new;
   p.v_new = v_new;
-  for (int i = 0; i < cfg->head_dim / 2; ++i)
-    p.inv_freq[i] = pow((double)rope_theta, -2.0 * i / (double)cfg->head_dim);
+  p.rope_tab = h->rope_tab;
   const bool fuse = !trie::attn_persist_enabled() && trie::attn_rope_fusable(p) &&
                     (((uintptr_t)q | (uintptr_t)k_new | (uintptr_t)v_new) & 3) == 0;
   if (!fuse) {  // two launches: rotate + append, then attention over the handle's trie
@@ -372,6 +374,14 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
     return trie_attn_decode(cfg, b_live, q, k_pool, v_pool, h->tlen, h->parent, h->depth, h->leaf,
                             h->n_nodes, h->mask, cfg->window, rows_hint, out, lse, scratch,
                             scratch_bytes, stream);
+  }
+  if (h->rope_tab_steps != h->steps || h->rope_tab_theta != rope_theta ||
+      h->rope_tab_blive != b_live) {  // once per step, shared by all layers
+    int rc = trie::launch_rope_table(h, rope_theta, stream);
+    if (rc) return rc;
+    h->rope_tab_steps = h->steps;
+    h->rope_tab_theta = rope_theta;
+    h->rope_tab_blive = b_live;
   }
   const AttnPlan pl = attn_plan(cfg, b_live, rows_hint, true);
   const size_t need = pl.counter_bytes + pl.part_bytes;

@@ -26,7 +26,7 @@ struct AttnParams {
   int rope;
   const void* k_new;      // [R][b_live][Hkv][D]
   const void* v_new;      // [R][b_live][Hkv][D]
-  double inv_freq[128];   // theta^(-2i/D), i < D/2 (host-computed in fp64)
+  const float2* rope_tab; // [R][b_live][D/2] (cos, sin) of the leaves' depths (per step)
 };
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);

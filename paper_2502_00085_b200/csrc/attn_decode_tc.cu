@@ -46,9 +46,7 @@ struct NarrowCfg {
   // epilogue staging [8*NQ][D+4] floats aliases the ring (all tiles consumed by then)
   static_assert(NQ * 8 * (D + 4) * 4 <= RG::RING_BYTES, "staging must fit in the ring");
   static constexpr int OFF_BAR = RG::RING_BYTES;
-  static constexpr int OFF_TAB = OFF_BAR + 128;  // fused RoPE: (cos, sin)[beam][D/2]
-  static constexpr int TAB = ROPE ? NQ * 8 * (D / 2) * 8 : 0;
-  static constexpr int SMEM = OFF_TAB + TAB + 1024;
+  static constexpr int SMEM = OFF_BAR + 128 + 1024;
   static_assert(2 * ST * 8 + 8 + (int)sizeof(ItemInfo) <= 128, "barrier area");
 };
 
@@ -66,7 +64,6 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
   uint64_t* empty = full + C::STAGES;
   uint64_t* app_done = empty + C::STAGES;
   ItemInfo* info = (ItemInfo*)(app_done + 1);
-  float2* cs_tab = (float2*)(smem + C::OFF_TAB);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -88,6 +85,40 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
                                     it.N - p.b_live);
       else
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+    } else if constexpr (ROPE) {
+      // lanes 1..31: write-before-read append (§3.4, Alg. 3 l.7) of the leaves whose slots
+      // lie in this CTA's tiles -- K rotated at the beam's depth with the step's (cos, sin)
+      // table, V copied -- then fence the generic writes for the TMA (async proxy) reads
+      // of lane 0, which waits on app_done only before the tile holding the first leaf.
+      const size_t mb = (size_t)r * p.cap;
+      (void)mb;
+      const int slot_lo = it.tile0 * TC_TR, slot_hi = (it.tile0 + it.ntiles) * TC_TR;
+      const __nv_bfloat16* kn = (const __nv_bfloat16*)p.k_new;
+      const __nv_bfloat16* vn = (const __nv_bfloat16*)p.v_new;
+      __nv_bfloat16* kpool = (__nv_bfloat16*)p.k;
+      __nv_bfloat16* vpool = (__nv_bfloat16*)p.v;
+      constexpr int HALF = D / 2;
+      for (int e = lane - 1; e < p.b_live * HALF; e += 31) {
+        const int j = e / HALF, i = e % HALF;
+        const int slot = p.leaf[r * TRIE_MAX_BEAMS + j];
+        if (slot < slot_lo || slot >= slot_hi) continue;
+        const __nv_bfloat16* src = kn + (((size_t)r * p.b_live + j) * p.Hkv + h) * D;
+        const float x1 = __bfloat162float(src[i]), x2 = __bfloat162float(src[i + HALF]);
+        const float2 c = p.rope_tab[((size_t)r * p.b_live + j) * HALF + i];
+        __nv_bfloat16* dst = kpool + (((size_t)r * p.Hkv + h) * p.cap + slot) * D;
+        dst[i] = __float2bfloat16_rn(x1 * c.x - x2 * c.y);
+        dst[i + HALF] = __float2bfloat16_rn(x2 * c.x + x1 * c.y);
+      }
+      for (int e = lane - 1; e < p.b_live * (D / 8); e += 31) {  // 16-byte V copies
+        const int j = e / (D / 8), d = (e % (D / 8)) * 8;
+        const int slot = p.leaf[r * TRIE_MAX_BEAMS + j];
+        if (slot < slot_lo || slot >= slot_hi) continue;
+        *(int4*)(vpool + (((size_t)r * p.Hkv + h) * p.cap + slot) * D + d) =
+            *(const int4*)(vn + (((size_t)r * p.b_live + j) * p.Hkv + h) * D + d);
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp(0xfffffffeu);
+      if (lane == 1) mbar_arrive(app_done);
     }
     return;
   }
@@ -96,46 +127,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
   const int gq = lane >> 2, cq = lane & 3;
   const size_t mbase = (size_t)r * p.cap;
   constexpr int HALF = D / 2;
-  if constexpr (ROPE) {
-    // (a) one angle per (beam, frequency): pos * theta^(-2i/D) in fp64, reduced mod 2*pi
-    //     in fp64, then fp32 sincos (reading R16; same positions as trie_rope_kv_append)
-    for (int e = lane; e < p.b_live * HALF; e += 32) {
-      const int j = e / HALF, i = e % HALF;
-      const double ang = (double)p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + j]] * p.inv_freq[i];
-      const double red = ang - rint(ang * 0.15915494309189535) * 6.283185307179586;
-      float sn, cs;
-      sincosf((float)red, &sn, &cs);
-      cs_tab[e] = make_float2(cs, sn);
-    }
-    __syncwarp();
-    // (b) write-before-read append of the leaves whose slots lie in this CTA's tiles
-    const int slot_lo = it.tile0 * TC_TR, slot_hi = (it.tile0 + it.ntiles) * TC_TR;
-    const __nv_bfloat16* kn = (const __nv_bfloat16*)p.k_new;
-    const __nv_bfloat16* vn = (const __nv_bfloat16*)p.v_new;
-    __nv_bfloat16* kpool = (__nv_bfloat16*)p.k;
-    __nv_bfloat16* vpool = (__nv_bfloat16*)p.v;
-    for (int e = lane; e < p.b_live * HALF; e += 32) {
-      const int j = e / HALF, i = e % HALF;
-      const int slot = p.leaf[r * TRIE_MAX_BEAMS + j];
-      if (slot < slot_lo || slot >= slot_hi) continue;
-      const __nv_bfloat16* src = kn + (((size_t)r * p.b_live + j) * p.Hkv + h) * D;
-      const float x1 = __bfloat162float(src[i]), x2 = __bfloat162float(src[i + HALF]);
-      const float2 c = cs_tab[e];
-      __nv_bfloat16* dst = kpool + (((size_t)r * p.Hkv + h) * p.cap + slot) * D;
-      dst[i] = __float2bfloat16_rn(x1 * c.x - x2 * c.y);
-      dst[i + HALF] = __float2bfloat16_rn(x2 * c.x + x1 * c.y);
-    }
-    for (int e = lane; e < p.b_live * D; e += 32) {
-      const int j = e / D, d = e % D;
-      const int slot = p.leaf[r * TRIE_MAX_BEAMS + j];
-      if (slot < slot_lo || slot >= slot_hi) continue;
-      vpool[(((size_t)r * p.Hkv + h) * p.cap + slot) * D + d] =
-          vn[(((size_t)r * p.b_live + j) * p.Hkv + h) * D + d];
-    }
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
-    __syncwarp();
-    if (lane == 0) mbar_arrive(app_done);
-  }
+  (void)HALF;
   // queries held by this thread in the S^T / O^T fragments: columns 2cq, 2cq+1 of each n-tile
   int beam[NQ][2], lod[NQ][2];
   bool qok[NQ][2];
@@ -172,7 +164,8 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
               const float2 x = __bfloat1622float2(*(const __nv_bfloat162*)&v);
               const float2 xp = __bfloat1622float2(*(const __nv_bfloat162*)&pv);
               const int i0 = d % HALF, j = m / g;
-              const float2 c0 = cs_tab[j * HALF + i0], c1 = cs_tab[j * HALF + i0 + 1];
+              const float2* tab = p.rope_tab + ((size_t)r * p.b_live + j) * HALF;
+              const float2 c0 = tab[i0], c1 = tab[i0 + 1];
               const float sg = d < HALF ? -1.f : 1.f;
               v = pack_bf16(x.x * c0.x + sg * xp.x * c0.y, x.y * c1.x + sg * xp.y * c1.y);
             }

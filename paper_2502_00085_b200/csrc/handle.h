@@ -34,6 +34,10 @@ struct trie_handle {
   int32_t* sel_parent = nullptr;  // [R][b]
   int32_t* sel_token = nullptr;   // [R][b]
   float* sel_score = nullptr;     // [R][b]
+  float2* rope_tab = nullptr;     // [R][b_live][D/2] (cos, sin) at the leaves' depths
+  int32_t rope_tab_steps = -1;    // host: step count the table was computed for
+  float rope_tab_theta = 0.f;
+  int32_t rope_tab_blive = 0;
   int32_t chunks = 1;
   int32_t chunk_len = 4096;
   // host-tracked state
@@ -55,6 +59,7 @@ int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t 
 int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, void* kpool,
                        void* vpool, float theta, cudaStream_t s);
 int launch_read_hyps(trie_handle* h, int32_t max_len, int32_t* out_dev, cudaStream_t s);
+int launch_rope_table(trie_handle* h, float theta, cudaStream_t s);
 int launch_mask_walk(const trie_cfg* cfg, int32_t b_live, const int32_t* tlen,
                      const int32_t* parent, const int32_t* leaf, const int32_t* nn,
                      uint32_t* mask_out, uint32_t* status, cudaStream_t s);

@@ -124,6 +124,28 @@ __global__ void __launch_bounds__(ROPE_BS) k_rope_append(
   }
 }
 
+// (cos, sin) of every live leaf's depth and frequency, once per step for all layers of
+// the fused trie_attn_decode_rope; same fp64 angle formula as k_rope_append (bit-equal).
+__global__ void k_rope_table(float2* __restrict__ tab, const int32_t* __restrict__ depth,
+                             const int32_t* __restrict__ leaf, int b_live, int D, int cap,
+                             double log2_theta) {
+  const int rj = blockIdx.x, r = rj / b_live, j = rj % b_live;
+  const int pos = depth[(size_t)r * cap + leaf[r * TRIE_MAX_BEAMS + j]];
+  for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
+    const double inv_freq = exp2(-2.0 * (double)i / (double)D * log2_theta);
+    double sn, cs;
+    sincos((double)pos * inv_freq, &sn, &cs);
+    tab[(size_t)rj * (D / 2) + i] = make_float2((float)cs, (float)sn);
+  }
+}
+
+int launch_rope_table(trie_handle* h, float theta, cudaStream_t s) {
+  const trie_cfg& c = h->cfg;
+  k_rope_table<<<c.n_requests * h->b_live, 64, 0, s>>>(h->rope_tab, h->depth, h->leaf, h->b_live,
+                                                       c.head_dim, c.capacity, log2((double)theta));
+  return trie_check_launch("k_rope_table");
+}
+
 int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, void* kpool,
                        void* vpool, float theta, cudaStream_t s) {
   const trie_cfg& c = h->cfg;
