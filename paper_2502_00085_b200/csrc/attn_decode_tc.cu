@@ -79,13 +79,23 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
   __syncthreads();
   const ItemInfo it = *info;
   if (warp == 0) {
-    if (lane == 0) {
-      if constexpr (ROPE)
+    if constexpr (ROPE) {
+      // fill the ring first (tiles that hold no leaf), then lane 0 streams the rest while
+      // lanes 1..31 append the leaves' K/V rows
+      const int first_leaf = it.N - p.b_live;
+      int fill = min(C::STAGES, it.ntiles);
+      while (fill > 0 && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
+      if (lane == 0)
+        producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr,
+                                    INT_MAX, 0, fill);
+      __syncwarp();
+      if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
-                                    it.N - p.b_live);
-      else
-        producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
-    } else if constexpr (ROPE) {
+                                    first_leaf, fill);
+    } else if (lane == 0) {
+      producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+    }
+    if constexpr (ROPE) if (lane != 0) {
       // lanes 1..31: write-before-read append (§3.4, Alg. 3 l.7) of the leaves whose slots
       // lie in this CTA's tiles -- K rotated at the beam's depth with the step's (cos, sin)
       // table, V copied -- then fence the generic writes for the TMA (async proxy) reads

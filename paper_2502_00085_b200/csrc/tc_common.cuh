@@ -146,12 +146,13 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
                                               const AttnParams& p, int r, int h,
                                               const ItemInfo& it, uint8_t* ring, uint64_t* full,
                                               uint64_t* empty, uint64_t* app_done = nullptr,
-                                              int first_leaf_slot = INT_MAX) {
+                                              int first_leaf_slot = INT_MAX, int i_begin = 0,
+                                              int i_end = INT_MAX) {
   using RG = Ring<D, STAGES>;
   const int row_base = (r * p.Hkv + h) * p.cap;
   const size_t mbase = (size_t)r * p.cap;
   bool appended = app_done == nullptr;
-  for (int i = 0; i < it.ntiles; ++i) {
+  for (int i = i_begin; i < min(it.ntiles, i_end); ++i) {
     const int s = i % STAGES;
     const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
     mbar_wait(&empty[s], ph ^ 1u);
