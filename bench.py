@@ -153,7 +153,10 @@ class HotPath:
         from paper_2502_00085_b200 import _lib
         self.plan = {var: _lib.trie_attn_plan_info(self.st.cfg, bl, self.rows_hint)
                      for var, bl in (("first", 1), ("steady", b))}
-        self.fused = {var: self.plan[var]["fused_rope"] for var in self.plan}
+        # trie_attn_decode_rope (one launch per layer) is opt-in: r07 measured 118.6 us per
+        # fused launch vs 112.7 us for trie_rope_kv_append + trie_attn_decode on Phi
+        self.fused = {var: self.plan[var]["fused_rope"] and os.environ.get("TRIE_BENCH_FUSED") == "1"
+                      for var in self.plan}
 
     def step_ops(self, var, slot, events=None):
         """Enqueue one step (all §8(a) rows) on the current stream."""

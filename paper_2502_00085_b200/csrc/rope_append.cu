@@ -56,21 +56,18 @@ constexpr int ROPE_BATCH = 4;
 template <typename T>
 __global__ void __launch_bounds__(ROPE_BS) k_rope_append(
     T* __restrict__ q, T* __restrict__ k_new, const T* __restrict__ v_new, T* __restrict__ kpool,
-    T* __restrict__ vpool, const int32_t* __restrict__ depth, const int32_t* __restrict__ leaf,
-    int b_live, int Hq, int Hkv, int D, int cap, double log2_theta) {
+    T* __restrict__ vpool, const int32_t* __restrict__ leaf, const float2* __restrict__ tab,
+    int b_live, int Hq, int Hkv, int D, int cap) {
   constexpr int VN = Vec16<T>::N;
   __shared__ float s_cos[128], s_sin[128];  // D <= 256
   const int rj = blockIdx.x;                // r * b_live + j
-  const int r = rj / b_live, j = rj % b_live;
-  const int slot = leaf[r * TRIE_MAX_BEAMS + j];
-  const int pos = depth[(size_t)r * cap + slot];
+  const int r = rj / b_live;
+  const int slot = leaf[r * TRIE_MAX_BEAMS + rj % b_live];
   const int half = D / 2;
-  for (int i = threadIdx.x; i < half; i += ROPE_BS) {
-    const double inv_freq = exp2(-2.0 * (double)i / (double)D * log2_theta);
-    double sn, cs;
-    sincos((double)pos * inv_freq, &sn, &cs);
-    s_cos[i] = (float)cs;
-    s_sin[i] = (float)sn;
+  for (int i = threadIdx.x; i < half; i += ROPE_BS) {  // the step's table (k_rope_table)
+    const float2 c = tab[(size_t)rj * half + i];
+    s_cos[i] = c.x;
+    s_sin[i] = c.y;
   }
   __syncthreads();
   const int cph = half / VN;                 // vector chunks per half-head
@@ -150,7 +147,13 @@ int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, 
                        void* vpool, float theta, cudaStream_t s) {
   const trie_cfg& c = h->cfg;
   const int grid = c.n_requests * h->b_live;
-  const double l2 = log2((double)theta);
+  if (h->rope_tab_steps != h->steps || h->rope_tab_theta != theta || h->rope_tab_blive != h->b_live) {
+    const int rc = launch_rope_table(h, theta, s);  // once per step, shared by all layers
+    if (rc) return rc;
+    h->rope_tab_steps = h->steps;
+    h->rope_tab_theta = theta;
+    h->rope_tab_blive = h->b_live;
+  }
   if ((((uintptr_t)q | (uintptr_t)k_new | (uintptr_t)v_new | (uintptr_t)kpool | (uintptr_t)vpool) & 15))
     return trie_set_error(TRIE_EINVAL, "rope_kv_append: buffers must be 16-byte aligned");
   if (c.kv_dtype == TRIE_BF16) {
@@ -158,13 +161,13 @@ int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, 
       return trie_set_error(TRIE_EINVAL, "rope_kv_append: bf16 needs head_dim % 16 == 0");
     k_rope_append<__nv_bfloat16><<<grid, ROPE_BS, 0, s>>>(
         (__nv_bfloat16*)q, (__nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
-        (__nv_bfloat16*)kpool, (__nv_bfloat16*)vpool, h->depth, h->leaf, h->b_live, c.n_q_heads,
-        c.n_kv_heads, c.head_dim, c.capacity, l2);
+        (__nv_bfloat16*)kpool, (__nv_bfloat16*)vpool, h->leaf, h->rope_tab, h->b_live,
+        c.n_q_heads, c.n_kv_heads, c.head_dim, c.capacity);
   } else {
     k_rope_append<float><<<grid, ROPE_BS, 0, s>>>((float*)q, (float*)k_new, (const float*)v_new,
-                                                  (float*)kpool, (float*)vpool, h->depth, h->leaf,
-                                                  h->b_live, c.n_q_heads, c.n_kv_heads,
-                                                  c.head_dim, c.capacity, l2);
+                                                  (float*)kpool, (float*)vpool, h->leaf,
+                                                  h->rope_tab, h->b_live, c.n_q_heads, c.n_kv_heads,
+                                                  c.head_dim, c.capacity);
   }
   return trie_check_launch("k_rope_append");
 }

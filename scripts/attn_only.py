@@ -61,6 +61,9 @@ def main():
         lambda: [(st.rope_kv_append(*d["views"][l], hp.kp[l], hp.vp[l], wl["theta"]),
                   st.attn_decode(d["views"][l][0], hp.kp[l], hp.vp[l], d["out"], rows_hint=hp.rows_hint))
                  for l in range(L)]) / L
+    res["fused_per_launch_us"] = 1e3 * time_graph(
+        lambda: [st.attn_decode_rope(*d["views"][l], hp.kp[l], hp.vp[l], wl["theta"], d["out"],
+                                     rows_hint=hp.rows_hint) for l in range(L)]) / L
     N = st.n_nodes.cpu().numpy()
     res["attn_bytes_per_launch"] = hp.attn_bytes(8, N)
     res["attn_only_GBps"] = res["attn_bytes_per_launch"] / (res["attn_only_per_launch_us"] * 1e-6) / 1e9
