@@ -243,8 +243,12 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo + several ranks per GPU is a test mode for boxes with fewer
+    # GPUs than ranks (the driver's runs use NCCL, one rank per GPU)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if rank == 0:
         build()
@@ -314,7 +318,7 @@ def run_gpu(args):
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
     if world > 1:
-        tt = torch.tensor([ms], device=dev)
+        tt = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     # Region B (roofline): the same K steps continued with the instrumented graphs (event
@@ -382,6 +386,9 @@ def run_gpu(args):
                             bound_b_ts_over_t_s_b_1=round(b * (t + k_star) / (t + k_star + b - 1), 3))
     if not args.no_e2e:
         res["e2e"] = run_e2e(hp, args, world)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     return res, dict(rank=rank, world=world)
 
 
@@ -441,7 +448,7 @@ def run_e2e(hp, args, world):
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
     if world > 1:
-        tt = torch.tensor([ms], device=hp.dev)
+        tt = torch.tensor([ms], device=hp.dev if os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     return {"value": round(hp.R * args.steps * world / (ms * 1e-3), 2), "unit": "request-steps/s",
