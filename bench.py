@@ -365,7 +365,7 @@ def run_gpu(args):
                                f"KV footprint ({kv_fp / 1e6:.0f} MB) > L2 (126 MB)")))
     res["roofline"] = dict(kernel="trie_attn_decode", bound="hbm", achieved=round(ach, 1), peak=peak,
                            unit="GB/s", frac=round(ach / peak, 4), frac_of_8TBps=round(ach / 8000, 4),
-                           traffic=_traffic(args.workload), peak_source=peak_src,
+                           traffic=_traffic(args.workload, R, b), peak_source=peak_src,
                            avg_launch_us=round(float(np.mean(attn_ms)) * 1e3, 2),
                            attn_share_of_step=round(float(np.sum(attn_ms)) / ms_b, 4),
                            timing="CUDA event nodes around every attention launch in a second timed "
@@ -458,13 +458,15 @@ def run_e2e(hp, args, world):
                     "double-buffered; selections device -> pinned host every step"}
 
 
-def _traffic(workload):
-    """dram bytes per attention launch from the committed ncu --set full summary, if any."""
+def _traffic(workload, R, b):
+    """dram bytes per attention launch from the committed ncu --set full summary, when it
+    was captured on this exact workload (same requests per GPU and beam width)."""
     p = os.path.join(ROOT, "profiles", "ncu_attn_summary.json")
     if os.path.exists(p):
         try:
-            d = json.load(open(p))
-            return d.get(workload, {}).get("dram_bytes_per_launch")
+            e = json.load(open(p)).get(workload, {})
+            if e.get("requests") == R and e.get("beam") == b:
+                return e.get("dram_bytes_per_launch")
         except Exception:
             return None
     return None
