@@ -106,9 +106,10 @@ struct UCfg {
   static constexpr int NBAR = 2 * ST + 2 + 2;  // full, empty, s_full[2], p_full, pv_done
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 64 + 1024;
   static constexpr int THREADS = 6 * 32;
-  static constexpr int COL_S0 = 0, COL_S1 = DB ? 64 : 0, COL_P = DB ? 128 : 64,
-                       COL_O = DB ? 160 : 96;
-  static constexpr int TMEM_COLS = DB ? 512 : 256;
+  // P (bf16, 32 columns) is written over the first half of the S buffer it was computed
+  // from, so S0 | S1 | O fit in 256 columns and two CTAs can share an SM's TMEM
+  static constexpr int COL_S0 = 0, COL_S1 = DB ? 64 : 0, COL_O = DB ? 128 : 64;
+  static constexpr int TMEM_COLS = 256;
   static_assert(COL_O + D <= TMEM_COLS, "TMEM budget");
 };
 
@@ -197,7 +198,8 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
           // V tile as MN-major B: 16 rows per K step = two 8-row atoms (1024 B); the
           // 32-column boxes are LBO = 4096 B apart, the 8-row atoms SBO = 512 B apart
           const uint64_t b = umma_desc_sw64(vb + kc * 1024, TC_TR * 64, 512);
-          umma_ts(tmem + C::COL_O, tmem + C::COL_P + kc * 8, b, idesc_pv, (i > 0 || kc > 0) ? 1u : 0u);
+          const uint32_t colp = (DB && (i & 1)) ? C::COL_S1 : C::COL_S0;  // P_i over S_i
+          umma_ts(tmem + C::COL_O, tmem + colp + kc * 8, b, idesc_pv, (i > 0 || kc > 0) ? 1u : 0u);
         }
         umma_commit(&empty[s]);
         umma_commit(pv_done);
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
           tmem_st32(tmem + lane_off + C::COL_O + c, o);
         }
       }
-      tmem_st32(tmem + lane_off + C::COL_P, pk);
+      tmem_st32(tmem + lane_off + ((DB && (i & 1)) ? C::COL_S1 : C::COL_S0), pk);  // P_i over S_i
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -427,7 +429,17 @@ static int umma_db() {
 }
 template <int D>
 static const UKernel& select_ud() {
-  if (umma_db()) return uk<D, 4, true>();
+  // TRIE_UMMA_ST: ring stages (default 2 -> two CTAs per SM with double-buffered S)
+  static int st = -1;
+  if (st < 0) {
+    const char* e = getenv("TRIE_UMMA_ST");
+    st = e ? atoi(e) : 2;
+  }
+  if (umma_db()) {
+    if (st >= 4) return uk<D, 4, true>();
+    if (st == 3) return uk<D, 3, true>();
+    return uk<D, 2, true>();
+  }
   return uk<D, 2, false>();
 }
 static const UKernel* select_u(int D) {
