@@ -94,35 +94,49 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2; ex2(-inf) = +0
   return y;
 }
 
-// DB: S double-buffered in TMEM (512 columns, 1 CTA/SM) or single-buffered (256 columns,
-// 2 CTAs/SM so two independent QK -> softmax -> PV chains share each SM).
-template <int D, int ST, bool DB>
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+
+// DB: S double-buffered in TMEM.  SW: softmax warps per TMEM sub-partition (1 or 2; with 2
+// the pair splits the 64 S columns and the D output columns, exchanging the row max
+// through shared memory once per tile).  P (bf16, 32 columns) overwrites the first half
+// of the S buffer it was computed from, so S0 | S1 | O fit in 256 TMEM columns.
+template <int D, int ST, bool DB, int SW>
 struct UCfg {
   using RG = Ring<D, ST>;
   static constexpr int STAGES = ST;
   static constexpr int QBYTES = 128 * D * 2;  // Q: 128 rows (padding zero), D/32 boxes
   static constexpr int OFF_Q = RG::RING_BYTES;
-  static constexpr int OFF_BAR = OFF_Q + QBYTES;
+  static constexpr int OFF_X = OFF_Q + QBYTES;           // row-max exchange [2][4][2][32] f32
+  static constexpr int OFF_BAR = OFF_X + 2 * 4 * 2 * 32 * 4;
   static constexpr int NBAR = 2 * ST + 2 + 2;  // full, empty, s_full[2], p_full, pv_done
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 64 + 1024;
-  static constexpr int THREADS = 6 * 32;
-  // P (bf16, 32 columns) is written over the first half of the S buffer it was computed
-  // from, so S0 | S1 | O fit in 256 columns and two CTAs can share an SM's TMEM
+  static constexpr int NSW = 4 * SW;           // softmax warps
+  static constexpr int THREADS = (2 + NSW) * 32;
+  static constexpr int CW = 64 / SW;           // S columns per softmax warp
+  static constexpr int OW = D / SW;            // O columns per softmax warp
   static constexpr int COL_S0 = 0, COL_S1 = DB ? 64 : 0, COL_O = DB ? 128 : 64;
   static constexpr int TMEM_COLS = 256;
   static_assert(COL_O + D <= TMEM_COLS, "TMEM budget");
+  static_assert(OW % 32 == 0, "O columns per warp");
 };
 
-template <int D, int ST, bool DB>
-__global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
+template <int D, int ST, bool DB, int SW>
+__global__ void __launch_bounds__(UCfg<D, ST, DB, SW>::THREADS) k_attn_umma(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p) {
-  using C = UCfg<D, ST, DB>;
+  using C = UCfg<D, ST, DB, SW>;
   using RG = typename C::RG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ring = smem;
   uint8_t* qsm = smem + C::OFF_Q;
+  float* xch = (float*)(smem + C::OFF_X);
   uint64_t* full = (uint64_t*)(smem + C::OFF_BAR);
   uint64_t* empty = full + ST;
   uint64_t* s_full = empty + ST;
@@ -141,7 +155,7 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
     }
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
-    mbar_init(p_full, 4);
+    mbar_init(p_full, C::NSW);
     mbar_init(pv_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     item_setup(p, r, split, info);
@@ -158,12 +172,13 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
   const ItemInfo it = *info;
   const uint32_t tmem = *tmem_slot;
   const int ntiles = it.ntiles;
+  constexpr int QBAR_THREADS = (C::NSW + 1) * 32;
 
   if (warp == 0) {
     if (lane == 0) producer_loop<D, ST>(&kmap, &vmap, p, r, h, it, ring, full, empty);
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    asm volatile("bar.sync 1, 160;");  // Q staged by the softmax warps
+    asm volatile("bar.sync 1, %0;" ::"r"(QBAR_THREADS));  // Q staged by the softmax warps
     tc_fence_after();
     const uint32_t idesc_qk = umma_idesc(128, 64, 0);
     const uint32_t idesc_pv = umma_idesc(128, D, 1);
@@ -193,12 +208,12 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
       if (lane == 0) {
         const int s = i % ST;
         const uint32_t vb = smem_u32(ring + s * RG::STAGE_BYTES + RG::TILE_BYTES);
+        const uint32_t colp = (DB && (i & 1)) ? C::COL_S1 : C::COL_S0;  // P_i over S_i
 #pragma unroll
         for (int kc = 0; kc < TC_TR / 16; ++kc) {
           // V tile as MN-major B: 16 rows per K step = two 8-row atoms (1024 B); the
           // 32-column boxes are LBO = 4096 B apart, the 8-row atoms SBO = 512 B apart
           const uint64_t b = umma_desc_sw64(vb + kc * 1024, TC_TR * 64, 512);
-          const uint32_t colp = (DB && (i & 1)) ? C::COL_S1 : C::COL_S0;  // P_i over S_i
           umma_ts(tmem + C::COL_O, tmem + colp + kc * 8, b, idesc_pv, (i > 0 || kc > 0) ? 1u : 0u);
         }
         umma_commit(&empty[s]);
@@ -219,14 +234,15 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
       }
     }
   } else {
-    // ===================== softmax / epilogue warps (2..5) =====================
+    // ===================== softmax / epilogue warps =====================
     const int sp = warp & 3;                  // TMEM sub-partition of this warp
+    const int half = (warp - 2) / 4;         // column half (SW = 2) / 0
     const int row = sp * 32 + lane;           // query row (MMA M index)
-    const int tid = threadIdx.x - 64;         // 0..127
+    const int tid = threadIdx.x - 64;
     {  // Q -> smem, 64B-swizzled K-major boxes of [128 rows][32 cols]; padding rows zero
       const __nv_bfloat16* q = (const __nv_bfloat16*)p.q;
       const int chunks = 128 * (D / 8);
-      for (int c = tid; c < chunks; c += 128) {
+      for (int c = tid; c < chunks; c += C::NSW * 32) {
         const int m = c / (D / 8), col = (c % (D / 8)) * 8;
         int4 v = make_int4(0, 0, 0, 0);
         if (m < Qg)
@@ -236,7 +252,7 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
         *(int4*)(qsm + box * 128 * 64 + (o ^ (((o >> 7) & 3u) << 4))) = v;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 1, 160;");
+      asm volatile("bar.sync 1, %0;" ::"r"(QBAR_THREADS));
     }
     const bool qvalid = row < Qg;
     const bool warp_live = sp * 32 < Qg;      // warp-uniform: all 32 rows padding -> skip math
@@ -246,6 +262,8 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
     const float sc = p.scale_log2;
     const int fast_end = min(it.t, it.N) / TC_TR;
     const uint32_t lane_off = (uint32_t)(sp * 32) << 16;
+    const int col0 = half * C::CW;            // this warp's S columns [col0, col0 + CW)
+    const int ocol0 = half * C::OW;           // this warp's O columns
     float m_run = -INFINITY, l_run = 0.f;
     for (int i = 0; i < ntiles; ++i) {
       const int s = i % ST;
@@ -253,33 +271,32 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
       mbar_wait(&s_full[DB ? (i & 1) : 0], spar);
       mbar_wait(&full[s], (uint32_t)(i / ST) & 1u);  // (complete) makes the mask words visible
       tc_fence_after();
-      uint32_t pk[32];
+      const uint32_t scol = (DB && (i & 1)) ? C::COL_S1 : C::COL_S0;
+      uint32_t pk[C::CW / 2];
       float alpha = 1.f;
       bool rescale = false;
       if (warp_live) {
-        uint32_t a[32], bq[32];
-        const uint32_t col = (DB && (i & 1)) ? C::COL_S1 : C::COL_S0;
-        tmem_ld32(tmem + lane_off + col, a);
-        tmem_ld32(tmem + lane_off + col + 32, bq);
-        tmem_wait_ld();
-        const int tile = it.tile0 + i;
-        const int n0 = tile * TC_TR;
-        const bool fast = tile >= it.fast_from && tile < fast_end;
-        float x[64];
-        const float scq = qvalid ? sc : 0.f;  // padding rows: every score -> -inf below
+        float x[C::CW];
+        {
+          uint32_t a[32];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          x[k] = qvalid ? __uint_as_float(a[k]) * scq : -INFINITY;
-          x[32 + k] = qvalid ? __uint_as_float(bq[k]) * scq : -INFINITY;
+          for (int c = 0; c < C::CW; c += 32) {
+            tmem_ld32(tmem + lane_off + scol + col0 + c, a);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) x[c + k] = qvalid ? __uint_as_float(a[k]) * sc : -INFINITY;
+          }
         }
-        if (!fast) {  // warp-uniform
+        const int tile = it.tile0 + i;
+        const int n0 = tile * TC_TR + col0;
+        if (!(tile >= it.fast_from && tile < fast_end)) {  // warp-uniform
           const uint8_t* stp = ring + s * RG::STAGE_BYTES;
-          const uint32_t* tmask = (const uint32_t*)(stp + 2 * RG::TILE_BYTES);
-          const int* tdep = (const int*)(stp + 2 * RG::TILE_BYTES + TC_TR * 4);
+          const uint32_t* tmask = (const uint32_t*)(stp + 2 * RG::TILE_BYTES) + col0;
+          const int* tdep = (const int*)(stp + 2 * RG::TILE_BYTES + TC_TR * 4) + col0;
 #pragma unroll
-          for (int k = 0; k < 64; ++k) {
+          for (int k = 0; k < C::CW; ++k) {
             const int n = n0 + k;
-            const bool ok = qvalid && n < it.N && (n < it.t || ((tmask[k] >> beam) & 1u)) && tdep[k] >= lod;
+            const bool ok = n < it.N && (n < it.t || ((tmask[k] >> beam) & 1u)) && tdep[k] >= lod;
             x[k] = ok ? x[k] : -INFINITY;
           }
         }
@@ -288,11 +305,17 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
         for (int u = 0; u < 8; ++u) {
           float v = x[u];
 #pragma unroll
-          for (int k = 8 + u; k < 64; k += 8) v = fmaxf(v, x[k]);
+          for (int k = 8 + u; k < C::CW; k += 8) v = fmaxf(v, x[k]);
           mx[u] = v;
         }
-        const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                           fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        if constexpr (SW == 2) {  // pair exchange of the row max (double-buffered by tile parity)
+          float* xb = xch + (i & 1) * 256 + sp * 64;
+          xb[half * 32 + lane] = tmax;
+          asm volatile("bar.sync %0, 64;" ::"r"(2 + sp));
+          tmax = fmaxf(tmax, xb[(1 - half) * 32 + lane]);
+        }
         // lazy rescale: keep the running max unless the tile max exceeds it by > 8 (log2)
         if (tmax > m_run + 8.f || (m_run == -INFINITY && tmax > -INFINITY)) {
           alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - tmax);
@@ -305,7 +328,7 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
 #pragma unroll
         for (int u = 0; u < 8; ++u) ps[u] = 0.f;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
+        for (int k = 0; k < C::CW / 2; ++k) {
           const float p0 = ex2(x[2 * k] - mu), p1 = ex2(x[2 * k + 1] - mu);
           ps[k & 7] += p0 + p1;
           pk[k] = pack_bf16(p0, p1);
@@ -313,7 +336,7 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
         l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       } else {
 #pragma unroll
-        for (int k = 0; k < 32; ++k) pk[k] = 0u;
+        for (int k = 0; k < C::CW / 2; ++k) pk[k] = 0u;
       }
       if (i > 0) {  // PV of the previous tile must be done before P / O are touched
         mbar_wait(pv_done, (uint32_t)(i - 1) & 1u);
@@ -321,16 +344,20 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
       }
       if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
-        for (int c = 0; c < D; c += 32) {
+        for (int c = 0; c < C::OW; c += 32) {
           uint32_t o[32];
-          tmem_ld32(tmem + lane_off + C::COL_O + c, o);
+          tmem_ld32(tmem + lane_off + C::COL_O + ocol0 + c, o);
           tmem_wait_ld();
 #pragma unroll
           for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
-          tmem_st32(tmem + lane_off + C::COL_O + c, o);
+          tmem_st32(tmem + lane_off + C::COL_O + ocol0 + c, o);
         }
       }
-      tmem_st32(tmem + lane_off + ((DB && (i & 1)) ? C::COL_S1 : C::COL_S0), pk);  // P_i over S_i
+      if constexpr (SW == 1) {
+        tmem_st32(tmem + lane_off + scol, *reinterpret_cast<uint32_t(*)[32]>(pk));  // P_i over S_i
+      } else {
+        tmem_st16(tmem + lane_off + scol + half * 16, pk);
+      }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -341,15 +368,24 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
       mbar_wait(pv_done, (uint32_t)(ntiles - 1) & 1u);
       tc_fence_after();
     }
+    if constexpr (SW == 2) {  // total row sum = both halves
+      float* xb = xch + 512 - 64 + sp * 16;  // last 64 floats of the exchange area... per sp
+      (void)xb;
+      float* lb = xch + sp * 64;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + sp));  // both done with the exchange buffers
+      lb[half * 32 + lane] = l_run;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + sp));
+      l_run += lb[(1 - half) * 32 + lane];
+    }
     const int j = beam, ii = row % g;
     if (warp_live) {
       if (p.splits == 1) {
-        __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
+        __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D + ocol0;
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
-        for (int c = 0; c < D; c += 32) {
+        for (int c = 0; c < C::OW; c += 32) {
           uint32_t o[32];
-          tmem_ld32(tmem + lane_off + C::COL_O + c, o);
+          tmem_ld32(tmem + lane_off + C::COL_O + ocol0 + c, o);
           tmem_wait_ld();
           if (qvalid) {
             uint32_t w[16];
@@ -361,7 +397,7 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
               *(int4*)(op + c + 8 * k) = make_int4((int)w[4 * k], (int)w[4 * k + 1], (int)w[4 * k + 2], (int)w[4 * k + 3]);
           }
         }
-        if (qvalid) {
+        if (qvalid && half == 0) {
           if (l_run == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
           if (p.lse)
             p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
@@ -370,17 +406,17 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB>::THREADS) k_attn_umma(
       } else {
         float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + row) * (D + 2);
 #pragma unroll
-        for (int c = 0; c < D; c += 32) {
+        for (int c = 0; c < C::OW; c += 32) {
           uint32_t o[32];
-          tmem_ld32(tmem + lane_off + C::COL_O + c, o);
+          tmem_ld32(tmem + lane_off + C::COL_O + ocol0 + c, o);
           tmem_wait_ld();
           if (qvalid) {
 #pragma unroll
             for (int k = 0; k < 32; k += 2)  // rows are (D + 2) floats: 8-byte aligned only
-              *(float2*)(pp + c + k) = make_float2(__uint_as_float(o[k]), __uint_as_float(o[k + 1]));
+              *(float2*)(pp + ocol0 + c + k) = make_float2(__uint_as_float(o[k]), __uint_as_float(o[k + 1]));
           }
         }
-        if (qvalid) {
+        if (qvalid && half == 0) {
           pp[D] = m_run;
           pp[D + 1] = l_run;
         }
@@ -403,11 +439,11 @@ struct UKernel {
   const void* fn;
   int smem, threads, occ;
 };
-template <int D, int ST, bool DB>
+template <int D, int ST, bool DB, int SW = 2>
 static const UKernel& uk() {
   static const UKernel k = [] {
-    using C = UCfg<D, ST, DB>;
-    auto kern = k_attn_umma<D, ST, DB>;
+    using C = UCfg<D, ST, DB, SW>;
+    auto kern = k_attn_umma<D, ST, DB, SW>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int occ = 0;
@@ -429,18 +465,27 @@ static int umma_db() {
 }
 template <int D>
 static const UKernel& select_ud() {
-  // TRIE_UMMA_ST: ring stages (default 2 -> two CTAs per SM with double-buffered S)
+  // TRIE_UMMA_ST: ring stages (default 4; r07: 2 stages x 2 CTAs/SM starve the ring)
   static int st = -1;
   if (st < 0) {
     const char* e = getenv("TRIE_UMMA_ST");
-    st = e ? atoi(e) : 2;
+    st = e ? atoi(e) : 4;
   }
-  if (umma_db()) {
-    if (st >= 4) return uk<D, 4, true>();
-    if (st == 3) return uk<D, 3, true>();
-    return uk<D, 2, true>();
+  static int sw = -1;  // TRIE_UMMA_SW: softmax warps per TMEM sub-partition (1 or 2)
+  if (sw < 0) {
+    const char* e = getenv("TRIE_UMMA_SW");
+    sw = e ? atoi(e) : 2;
   }
-  return uk<D, 2, false>();
+  if (sw == 1) {
+    if (st >= 4) return uk<D, 4, true, 1>();
+    if (st == 3) return uk<D, 3, true, 1>();
+    return uk<D, 2, true, 1>();
+  }
+  constexpr int SW2 = (D % 64 == 0) ? 2 : 1;  // D = 96: 48 O columns per warp -> SW = 1
+  if (!umma_db()) return uk<D, 2, false, SW2>();
+  if (st >= 4) return uk<D, 4, true, SW2>();
+  if (st == 3) return uk<D, 3, true, SW2>();
+  return uk<D, 2, true, SW2>();
 }
 static const UKernel* select_u(int D) {
   switch (D) {
