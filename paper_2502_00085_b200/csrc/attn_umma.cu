@@ -483,6 +483,7 @@ static const UKernel& select_ud() {
   }
   constexpr int SW2 = (D % 64 == 0) ? 2 : 1;  // D = 96: 48 O columns per warp -> SW = 1
   if (!umma_db()) return uk<D, 2, false, SW2>();
+  if (st >= 5 && UCfg<D, 5, true, SW2>::SMEM <= 227 * 1024) return uk<D, (D <= 128 ? 5 : 4), true, SW2>();
   if (st >= 4) return uk<D, 4, true, SW2>();
   if (st == 3) return uk<D, 3, true, SW2>();
   return uk<D, 2, true, SW2>();
