@@ -21,6 +21,8 @@ FLAGS = [
     "--expt-relaxed-constexpr", "-Xptxas", "-v",
     "-I" + os.path.join(ROOT, "include"),
 ]
+# experiment builds: TRIE_BUILD_DEFINES="TRIE_UMMA_TRACE=1" (use --force; see scripts/umma_trace.py)
+FLAGS += ["-D" + d for d in os.environ.get("TRIE_BUILD_DEFINES", "").split() if d]
 OBJDIR = os.path.join(HERE, "build_obj")
 
 

@@ -10,11 +10,16 @@
 //                                             MN-major SW64; fp32 in TMEM)
 // The TMA tiles written by the producer ARE the canonical UMMA layouts (64-byte rows,
 // 8-row atoms of 512 B, 32-column boxes 4096 B apart), so no re-staging is needed.
-// Warp roles: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..5 = softmax /
-// epilogue (warp w reads TMEM lanes 32*(w%4).., thread = query row).  S is double
-// buffered so QK of tile i+1 overlaps the softmax of tile i; the running max is rescaled
-// lazily (O is only rescaled when a row max grows by > 8 in log2 units).
-// Rows >= Qg of the 128-row MMA are padding (Q rows zero, P rows zero, outputs ignored).
+// Warp roles: 0 = TMA producer, 1 = TMEM allocator + PV issuer, 2 = QK issuer, 3..10 =
+// softmax / epilogue in two groups by tile parity: group e (warps 3+4e .. 6+4e) owns the
+// even (e = 0) or odd (e = 1) tiles and its own accumulator O_e with its own running max
+// and sum; a thread owns one query row (TMEM lane = warp % 4 quarter)
+// and all 64 columns of its tiles.  The two warps on an SMSP work on consecutive tiles, so
+// one's exp2 phase (MUFU) overlaps the other's TMEM load / mask / max phase (r09 trace: a
+// single group ran load 200 + max 320 + exp 700 cycles per tile back to back).  O_0 and
+// O_1 are merged once at the end (the in-CTA analogue of the split-K combine).  The
+// running max is rescaled lazily (only when a row max grows by > 8 in log2 units).
+// Rows >= Qg of the 128-row MMA are padding (Q rows zero; their warps skip the softmax).
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -94,6 +99,19 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2; ex2(-inf) = +0
   return y;
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -102,61 +120,78 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
       "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
 }
 
-// DB: S double-buffered in TMEM.  SW: softmax warps per TMEM sub-partition (1 or 2; with 2
-// the pair splits the 64 S columns and the D output columns, exchanging the row max
-// through shared memory once per tile).  P (bf16, 32 columns) overwrites the first half
-// of the S buffer it was computed from, so S0 | S1 | O fit in 256 TMEM columns.
-template <int D, int ST, bool DB, int SW>
+// S_0..S_3 | O_0 | O_1 in TMEM: tile i uses S_{i%4} (so QK(i+2) never waits for PV(i):
+// r10 trace, with two S buffers each group idled ~1.1k cycles per tile on that chain);
+// P (bf16, 32 columns) overwrites the first half of the S buffer it was computed from.
+// K and V have separate rings with their own producers: a K tile is free as soon as QK(i)
+// completes, a V tile (+ the tile's mask / depth words) only after PV(i), i.e. after the
+// softmax; r10 trace: with one 33 KB stage ring the stages were held ~1.7k cycles by the
+// consumers and only ~2.4 of 4 were in flight against a ~2.6k-cycle TMA latency.
+template <int D, int STK, int STV>
 struct UCfg {
-  using RG = Ring<D, ST>;
-  static constexpr int STAGES = ST;
+  static_assert(STV % 2 == 0 && STV >= 4, "V stage s serves one tile parity; STV >= NSB");
+  static constexpr int TILE = TC_TR * D * 2;    // one K or V tile: D/32 boxes of 64 x 64 B
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + STK * TILE;
+  static constexpr int OFF_MD = OFF_V + STV * TILE;  // [STV][mask 64 x u32 | depth 64 x i32]
   static constexpr int QBYTES = 128 * D * 2;  // Q: 128 rows (padding zero), D/32 boxes
-  static constexpr int OFF_Q = RG::RING_BYTES;
-  static constexpr int OFF_X = OFF_Q + QBYTES;           // row-max exchange [2][4][2][32] f32
-  static constexpr int OFF_BAR = OFF_X + 2 * 4 * 2 * 32 * 4;
-  static constexpr int NBAR = 2 * ST + 2 + 2;  // full, empty, s_full[2], p_full, pv_done
+  static constexpr int OFF_Q = (OFF_MD + STV * 512 + 1023) / 1024 * 1024;
+  static constexpr int OFF_X = OFF_Q + QBYTES;           // epilogue (m, l) exchange [2][4][32] f32x2
+  static constexpr int OFF_BAR = OFF_X + 2 * 4 * 32 * 8;
+  static constexpr int NSB = 4;                    // S buffers
+  static constexpr int NBAR = 2 * STK + 2 * STV + 3 * NSB;  // K/V full/empty, s_full, p_full, pv_done
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 64 + 1024;
-  static constexpr int NSW = 4 * SW;           // softmax warps
-  static constexpr int THREADS = (2 + NSW) * 32;
-  static constexpr int CW = 64 / SW;           // S columns per softmax warp
-  static constexpr int OW = D / SW;            // O columns per softmax warp
-  static constexpr int COL_S0 = 0, COL_S1 = DB ? 64 : 0, COL_O = DB ? 128 : 64;
-  static constexpr int TMEM_COLS = 256;
-  static_assert(COL_O + D <= TMEM_COLS, "TMEM budget");
-  static_assert(OW % 32 == 0, "O columns per warp");
+  static constexpr int NSW = 8;                // softmax warps (2 groups x 4 sub-partitions)
+  static constexpr int THREADS = (4 + NSW) * 32; // + K producer, PV, QK, V producer (last)
+  static constexpr int COL_O0 = 64 * NSB, COL_O1 = 64 * NSB + D;
+  static constexpr int TMEM_COLS = 512;
+  static_assert(64 * NSB + 2 * D <= TMEM_COLS, "TMEM budget");
+  static_assert(D % 32 == 0, "head_dim");
 };
 
-template <int D, int ST, bool DB, int SW>
-__global__ void __launch_bounds__(UCfg<D, ST, DB, SW>::THREADS) k_attn_umma(
+#ifndef TRIE_UMMA_TRACE
+#define TRIE_UMMA_TRACE 0
+#endif
+
+template <int D, int STK, int STV>
+__global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p) {
-  using C = UCfg<D, ST, DB, SW>;
-  using RG = typename C::RG;
+  using C = UCfg<D, STK, STV>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* ring = smem;
   uint8_t* qsm = smem + C::OFF_Q;
-  float* xch = (float*)(smem + C::OFF_X);
-  uint64_t* full = (uint64_t*)(smem + C::OFF_BAR);
-  uint64_t* empty = full + ST;
-  uint64_t* s_full = empty + ST;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* pv_done = p_full + 1;
-  uint32_t* tmem_slot = (uint32_t*)(pv_done + 1);
+  float2* xch = (float2*)(smem + C::OFF_X);
+  uint64_t* fullK = (uint64_t*)(smem + C::OFF_BAR);
+  uint64_t* emptyK = fullK + STK;
+  uint64_t* fullV = emptyK + STK;
+  uint64_t* emptyV = fullV + STV;
+  uint64_t* s_full = emptyV + STV;
+  uint64_t* p_full = s_full + C::NSB;
+  uint64_t* pv_done = p_full + C::NSB;
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + C::NSB);
   ItemInfo* info = (ItemInfo*)(tmem_slot + 4);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
+  const int n_live = min(4, (Qg + 31) / 32);  // sub-partitions holding real query rows
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < STK; ++s) {
+      mbar_init(&fullK[s], 1);
+      mbar_init(&emptyK[s], 1);
     }
-    mbar_init(&s_full[0], 1);
-    mbar_init(&s_full[1], 1);
-    mbar_init(p_full, C::NSW);
-    mbar_init(pv_done, 1);
+    for (int s = 0; s < STV; ++s) {
+      mbar_init(&fullV[s], 1);
+      mbar_init(&emptyV[s], 1);
+    }
+    // one (s_full, p_full, pv_done) triple per S buffer: a barrier's next phase always
+    // needs the waiter's own progress first, so no wait can alias a later phase
+    for (int e = 0; e < C::NSB; ++e) {
+      mbar_init(&s_full[e], 1);
+      mbar_init(&p_full[e], n_live);  // the live softmax warps of the tile's group
+      mbar_init(&pv_done[e], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     item_setup(p, r, split, info);
   }
@@ -172,73 +207,113 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB, SW>::THREADS) k_attn_umma(
   const ItemInfo it = *info;
   const uint32_t tmem = *tmem_slot;
   const int ntiles = it.ntiles;
+#if TRIE_UMMA_TRACE
+  // CTA (0,0,0) records clock() per tile into p.out (build with TRIE_UMMA_TRACE=1;
+  // scripts/umma_trace.py; results are not written)
+  uint32_t* trc = (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? (uint32_t*)p.out : nullptr;
+#define TRC(i, k) do { if (trc && (i) < 400) trc[(i) * 16 + (k)] = (uint32_t)clock(); } while (0)
+#else
+  uint32_t* trc = nullptr;
+#define TRC(i, k) do { } while (0)
+#endif
   constexpr int QBAR_THREADS = (C::NSW + 1) * 32;
 
-  if (warp == 0) {
-    if (lane == 0) producer_loop<D, ST>(&kmap, &vmap, p, r, h, it, ring, full, empty);
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    asm volatile("bar.sync 1, %0;" ::"r"(QBAR_THREADS));  // Q staged by the softmax warps
-    tc_fence_after();
+  if (warp == 0 || warp == 3 + C::NSW) {
+    // ============ TMA producers: warp 0 = K tiles, the last warp = V tiles + mask words ============
+    if (lane == 0) {
+      const bool isv = warp != 0;
+      const int row_base = (r * p.Hkv + h) * p.cap;
+      const size_t mbase = (size_t)r * p.cap;
+      const int ns = isv ? STV : STK;
+      uint64_t* fb = isv ? fullV : fullK;
+      uint64_t* eb = isv ? emptyV : emptyK;
+      const CUtensorMap* map = isv ? &vmap : &kmap;
+      const uint32_t base = smem_u32(smem + (isv ? C::OFF_V : C::OFF_K));
+      for (int i = 0; i < ntiles; ++i) {
+        const int s = i % ns;
+        mbar_wait(&eb[s], ((uint32_t)(i / ns) & 1u) ^ 1u);
+        TRC(i, isv ? 12 : 7);
+        const int n0 = (it.tile0 + i) * TC_TR;
+        // mask / depth words clamped to the [R][cap] arrays (cap % 4 == 0: 16-byte granules)
+        const uint32_t mdb = isv ? (uint32_t)min(TC_TR, p.cap - n0) * 4u : 0u;
+        mbar_expect_tx(&fb[s], C::TILE + 2 * mdb);
+#pragma unroll
+        for (int bx = 0; bx < D / TC_CW; ++bx)
+          tma_load_2d(base + s * C::TILE + bx * TC_TR * 64, map, bx * TC_CW, row_base + n0, &fb[s]);
+        if (isv) {
+          const uint32_t md = smem_u32(smem + C::OFF_MD + s * 512);
+          bulk_load_1d(md, p.mask + mbase + n0, mdb, &fb[s]);
+          bulk_load_1d(md + 256, p.depth + mbase + n0, mdb, &fb[s]);
+        }
+        TRC(i, isv ? 13 : 8);
+      }
+    }
+  } else if (warp <= 2) {
+    // ============ MMA issuers: warp 2 = QK (needs Q), warp 1 = PV ============
+    // Two issuing warps so that PV(i) (which releases ring stage i) never queues behind the
+    // wait for tile i+1's data that QK(i+1) needs (r08 trace: with one issuer the stage was
+    // released ~1.7k cycles late).  QK(i) overwrites S_{i%4}, which holds P_{i-4}: it waits
+    // for PV(i-4).  Each warp commits only its own MMAs.
     const uint32_t idesc_qk = umma_idesc(128, 64, 0);
     const uint32_t idesc_pv = umma_idesc(128, D, 1);
-    const uint32_t qbase = smem_u32(qsm);
-    auto issue_qk = [&](int i) {
-      const int s = i % ST;
-      mbar_wait(&full[s], (uint32_t)(i / ST) & 1u);
+    if (warp == 2) {
+      asm volatile("bar.sync 1, %0;" ::"r"(QBAR_THREADS));  // Q staged by the softmax warps
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t kb = smem_u32(ring + s * RG::STAGE_BYTES);
-        const uint32_t d_s = tmem + ((i & 1) ? C::COL_S1 : C::COL_S0);
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          // K step ks: 32-column box ks/2 (8 KB apart for the 128-row Q, 4 KB for the 64-row
-          // K tile), + 32 B inside the 64-byte swizzled row for odd steps; SBO = 8 rows = 512 B
-          const uint64_t a = umma_desc_sw64(qbase + (ks >> 1) * 128 * 64 + (ks & 1) * 32, 16, 512);
-          const uint64_t b = umma_desc_sw64(kb + (ks >> 1) * TC_TR * 64 + (ks & 1) * 32, 16, 512);
-          umma_ss(d_s, a, b, idesc_qk, ks > 0);
-        }
-        umma_commit(&s_full[DB ? (i & 1) : 0]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int i) {
-      mbar_wait(p_full, (uint32_t)i & 1u);
-      tc_fence_after();
-      if (lane == 0) {
-        const int s = i % ST;
-        const uint32_t vb = smem_u32(ring + s * RG::STAGE_BYTES + RG::TILE_BYTES);
-        const uint32_t colp = (DB && (i & 1)) ? C::COL_S1 : C::COL_S0;  // P_i over S_i
-#pragma unroll
-        for (int kc = 0; kc < TC_TR / 16; ++kc) {
-          // V tile as MN-major B: 16 rows per K step = two 8-row atoms (1024 B); the
-          // 32-column boxes are LBO = 4096 B apart, the 8-row atoms SBO = 512 B apart
-          const uint64_t b = umma_desc_sw64(vb + kc * 1024, TC_TR * 64, 512);
-          umma_ts(tmem + C::COL_O, tmem + colp + kc * 8, b, idesc_pv, (i > 0 || kc > 0) ? 1u : 0u);
-        }
-        umma_commit(&empty[s]);
-        umma_commit(pv_done);
-      }
-      __syncwarp();
-    };
-    if constexpr (DB) {
-      if (ntiles > 0) issue_qk(0);
+      const uint32_t qbase = smem_u32(qsm);
       for (int i = 0; i < ntiles; ++i) {
-        if (i + 1 < ntiles) issue_qk(i + 1);  // overlaps the softmax of tile i
-        issue_pv(i);
+        const int s = i % STK;
+        const int sb = i % C::NSB;
+        if (i >= C::NSB) mbar_wait(&pv_done[sb], (uint32_t)((i - C::NSB) / C::NSB) & 1u);
+        mbar_wait(&fullK[s], (uint32_t)(i / STK) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          TRC(i, 5);
+          const uint32_t kb = smem_u32(smem + C::OFF_K + s * C::TILE);
+          const uint32_t d_s = tmem + sb * 64;
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            // K step ks: 32-column box ks/2 (8 KB apart for the 128-row Q, 4 KB for the 64-row
+            // K tile), + 32 B inside the 64-byte swizzled row for odd steps; SBO = 8 rows = 512 B
+            const uint64_t a = umma_desc_sw64(qbase + (ks >> 1) * 128 * 64 + (ks & 1) * 32, 16, 512);
+            const uint64_t b = umma_desc_sw64(kb + (ks >> 1) * TC_TR * 64 + (ks & 1) * 32, 16, 512);
+            umma_ss(d_s, a, b, idesc_qk, ks > 0);
+          }
+          umma_commit(&s_full[sb]);
+          umma_commit(&emptyK[s]);  // K tile free once QK(i) has read it
+        }
+        __syncwarp();
       }
     } else {
-      for (int i = 0; i < ntiles; ++i) {  // S is reused: QK(i+1) waits for softmax(i)
-        issue_qk(i);
-        issue_pv(i);
+      for (int i = 0; i < ntiles; ++i) {
+        const int sb = i % C::NSB, s = i % STV;
+        mbar_wait(&p_full[sb], (uint32_t)(i / C::NSB) & 1u);
+        if (lane == 0) TRC(i, 6);
+        mbar_wait(&fullV[s], (uint32_t)(i / STV) & 1u);
+        tc_fence_after();
+        if (lane == 0) {
+          TRC(i, 14);
+          const uint32_t vb = smem_u32(smem + C::OFF_V + s * C::TILE);
+          const uint32_t colp = sb * 64;                          // P_i over S_i
+          const uint32_t colo = (i & 1) ? C::COL_O1 : C::COL_O0;  // group accumulator
+#pragma unroll
+          for (int kc = 0; kc < TC_TR / 16; ++kc) {
+            // V tile as MN-major B: 16 rows per K step = two 8-row atoms (1024 B); the
+            // 32-column boxes are LBO = 4096 B apart, the 8-row atoms SBO = 512 B apart
+            const uint64_t b = umma_desc_sw64(vb + kc * 1024, TC_TR * 64, 512);
+            umma_ts(tmem + colo, tmem + colp + kc * 8, b, idesc_pv, (i >= 2 || kc > 0) ? 1u : 0u);
+          }
+          umma_commit(&emptyV[s]);
+          umma_commit(&pv_done[sb]);
+        }
+        __syncwarp();
       }
     }
   } else {
     // ===================== softmax / epilogue warps =====================
     const int sp = warp & 3;                  // TMEM sub-partition of this warp
-    const int half = (warp - 2) / 4;         // column half (SW = 2) / 0
+    const int grp = (warp - 3) / 4;           // tile parity this warp handles
     const int row = sp * 32 + lane;           // query row (MMA M index)
-    const int tid = threadIdx.x - 64;
+    const int tid = threadIdx.x - 96;
     {  // Q -> smem, 64B-swizzled K-major boxes of [128 rows][32 cols]; padding rows zero
       const __nv_bfloat16* q = (const __nv_bfloat16*)p.q;
       const int chunks = 128 * (D / 8);
@@ -254,47 +329,51 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB, SW>::THREADS) k_attn_umma(
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"r"(QBAR_THREADS));
     }
-    const bool qvalid = row < Qg;
-    const bool warp_live = sp * 32 < Qg;      // warp-uniform: all 32 rows padding -> skip math
-    const int beam = qvalid ? row / g : 0;
-    const size_t mbase = (size_t)r * p.cap;
-    const int lod = (p.window > 0 && qvalid) ? p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam]] - p.window + 1 : INT_MIN;
-    const float sc = p.scale_log2;
-    const int fast_end = min(it.t, it.N) / TC_TR;
-    const uint32_t lane_off = (uint32_t)(sp * 32) << 16;
-    const int col0 = half * C::CW;            // this warp's S columns [col0, col0 + CW)
-    const int ocol0 = half * C::OW;           // this warp's O columns
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int i = 0; i < ntiles; ++i) {
-      const int s = i % ST;
-      const uint32_t spar = DB ? ((uint32_t)(i >> 1) & 1u) : ((uint32_t)i & 1u);
-      mbar_wait(&s_full[DB ? (i & 1) : 0], spar);
-      mbar_wait(&full[s], (uint32_t)(i / ST) & 1u);  // (complete) makes the mask words visible
-      tc_fence_after();
-      const uint32_t scol = (DB && (i & 1)) ? C::COL_S1 : C::COL_S0;
-      uint32_t pk[C::CW / 2];
-      float alpha = 1.f;
-      bool rescale = false;
-      if (warp_live) {
-        float x[C::CW];
+    if (sp < n_live) {  // warps of padding-only sub-partitions have nothing to do
+      const bool qvalid = row < Qg;
+      const int beam = qvalid ? row / g : 0;
+      const size_t mbase = (size_t)r * p.cap;
+      const int lod = (p.window > 0 && qvalid) ? p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam]] - p.window + 1 : INT_MIN;
+      const float sc = p.scale_log2;
+      const int fast_end = min(it.t, it.N) / TC_TR;
+      const uint32_t lane_off = (uint32_t)(sp * 32) << 16;
+      const uint32_t ocol = grp ? C::COL_O1 : C::COL_O0;
+      const bool tr = trc && (warp == 4 || warp == 8) && lane == 0;  // sub-partition 0, both groups
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int i = grp; i < ntiles; i += 2) {
+        const int sb = i % C::NSB;
+        const uint32_t scol = sb * 64;
+        const int tile = it.tile0 + i;
+        const bool slow = !(tile >= it.fast_from && tile < fast_end);  // warp-uniform
+        if (tr) TRC(i, 0);
+        mbar_wait(&s_full[sb], (uint32_t)(i / C::NSB) & 1u);
+        if (tr) TRC(i, 1);
+        // the V transaction carries the tile's mask / depth words.  Skipping its phase on
+        // fast tiles is safe: s_full(i) implies PV(i-4), hence fullV(i-4) and every earlier
+        // phase of this stage, complete (STV >= 4), so the wait below never aliases
+        if (slow) mbar_wait(&fullV[i % STV], (uint32_t)(i / STV) & 1u);
+        tc_fence_after();
+        if (tr) TRC(i, 2);
+        // raw S (the scale is folded into the exponent FFMA)
+        float x[64];
         {
           uint32_t a[32];
+          tmem_ld32(tmem + lane_off + scol, a);
+          tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < C::CW; c += 32) {
-            tmem_ld32(tmem + lane_off + scol + col0 + c, a);
-            tmem_wait_ld();
+          for (int k = 0; k < 32; ++k) x[k] = __uint_as_float(a[k]);
+          tmem_ld32(tmem + lane_off + scol + 32, a);
+          tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 32; ++k) x[c + k] = qvalid ? __uint_as_float(a[k]) * sc : -INFINITY;
-          }
+          for (int k = 0; k < 32; ++k) x[32 + k] = __uint_as_float(a[k]);
         }
-        const int tile = it.tile0 + i;
-        const int n0 = tile * TC_TR + col0;
-        if (!(tile >= it.fast_from && tile < fast_end)) {  // warp-uniform
-          const uint8_t* stp = ring + s * RG::STAGE_BYTES;
-          const uint32_t* tmask = (const uint32_t*)(stp + 2 * RG::TILE_BYTES) + col0;
-          const int* tdep = (const int*)(stp + 2 * RG::TILE_BYTES + TC_TR * 4) + col0;
+        if (tr) TRC(i, 9);
+        const int n0 = tile * TC_TR;
+        if (slow) {
+          const uint32_t* tmask = (const uint32_t*)(smem + C::OFF_MD + (i % STV) * 512);
+          const int* tdep = (const int*)(smem + C::OFF_MD + (i % STV) * 512 + TC_TR * 4);
 #pragma unroll
-          for (int k = 0; k < C::CW; ++k) {
+          for (int k = 0; k < 64; ++k) {
             const int n = n0 + k;
             const bool ok = n < it.N && (n < it.t || ((tmask[k] >> beam) & 1u)) && tdep[k] >= lod;
             x[k] = ok ? x[k] : -INFINITY;
@@ -305,17 +384,15 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB, SW>::THREADS) k_attn_umma(
         for (int u = 0; u < 8; ++u) {
           float v = x[u];
 #pragma unroll
-          for (int k = 8 + u; k < C::CW; k += 8) v = fmaxf(v, x[k]);
+          for (int k = 8 + u; k < 64; k += 8) v = fmaxf(v, x[k]);
           mx[u] = v;
         }
         float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                            fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        if constexpr (SW == 2) {  // pair exchange of the row max (double-buffered by tile parity)
-          float* xb = xch + (i & 1) * 256 + sp * 64;
-          xb[half * 32 + lane] = tmax;
-          asm volatile("bar.sync %0, 64;" ::"r"(2 + sp));
-          tmax = fmaxf(tmax, xb[(1 - half) * 32 + lane]);
-        }
+        if (tr) TRC(i, 10);
+        tmax *= sc;  // log2 units (sc > 0: the max commutes with the scaling)
+        float alpha = 1.f;
+        bool rescale = false;
         // lazy rescale: keep the running max unless the tile max exceeds it by > 8 (log2)
         if (tmax > m_run + 8.f || (m_run == -INFINITY && tmax > -INFINITY)) {
           alpha = (m_run == -INFINITY) ? 0.f : ex2(m_run - tmax);
@@ -323,106 +400,132 @@ __global__ void __launch_bounds__(UCfg<D, ST, DB, SW>::THREADS) k_attn_umma(
           m_run = tmax;
           l_run *= alpha;
         }
-        const float mu = m_run == -INFINITY ? 0.f : m_run;  // all masked: ex2(-inf) = 0
+        const float nmu = m_run == -INFINITY ? 0.f : -m_run;  // all masked: ex2(-inf) = 0
+        uint32_t pk[32];
         float ps[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) ps[u] = 0.f;
 #pragma unroll
-        for (int k = 0; k < C::CW / 2; ++k) {
-          const float p0 = ex2(x[2 * k] - mu), p1 = ex2(x[2 * k + 1] - mu);
+        for (int k = 0; k < 32; ++k) {
+          const float p0 = ex2(fmaf(x[2 * k], sc, nmu)), p1 = ex2(fmaf(x[2 * k + 1], sc, nmu));
           ps[k & 7] += p0 + p1;
           pk[k] = pack_bf16(p0, p1);
         }
         l_run += ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-      } else {
+        if (tr) TRC(i, 11);
+        // P_i overwrites S_i, whose previous occupant P_{i-4} was read by PV(i-4) before
+        // QK(i) was issued.  Only an O_grp rescale (rare) waits for this group's last PV.
+        if (__any_sync(0xffffffffu, rescale)) {
+          if (i >= 2) {
+            mbar_wait(&pv_done[(i - 2) % C::NSB], (uint32_t)((i - 2) / C::NSB) & 1u);
+            tc_fence_after();
+          }
 #pragma unroll
-        for (int k = 0; k < C::CW / 2; ++k) pk[k] = 0u;
+          for (int c = 0; c < D; c += 32) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lane_off + ocol + c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
+            tmem_st32(tmem + lane_off + ocol + c, o);
+          }
+        }
+        if (tr) TRC(i, 3);
+        tmem_st32(tmem + lane_off + scol, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[sb]);
+        if (tr) TRC(i, 4);
       }
-      if (i > 0) {  // PV of the previous tile must be done before P / O are touched
-        mbar_wait(pv_done, (uint32_t)(i - 1) & 1u);
+      // ---- epilogue: merge (O_0, m_0, l_0) and (O_1, m_1, l_1); group e writes columns
+      // [e*D/2, (e+1)*D/2) of every row of its sub-partition ----
+      const int last = ((ntiles - 1 - grp) >> 1) * 2 + grp;  // this group's last tile
+      if (last >= 0 && last < ntiles) {
+        mbar_wait(&pv_done[last % C::NSB], (uint32_t)(last / C::NSB) & 1u);
         tc_fence_after();
       }
-      if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll
-        for (int c = 0; c < C::OW; c += 32) {
-          uint32_t o[32];
-          tmem_ld32(tmem + lane_off + C::COL_O + ocol0 + c, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * alpha);
-          tmem_st32(tmem + lane_off + C::COL_O + ocol0 + c, o);
-        }
-      }
-      if constexpr (SW == 1) {
-        tmem_st32(tmem + lane_off + scol, *reinterpret_cast<uint32_t(*)[32]>(pk));  // P_i over S_i
-      } else {
-        tmem_st16(tmem + lane_off + scol + half * 16, pk);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-    }
-    // ---- epilogue: O / l ----
-    if (ntiles > 0) {
-      mbar_wait(pv_done, (uint32_t)(ntiles - 1) & 1u);
-      tc_fence_after();
-    }
-    if constexpr (SW == 2) {  // total row sum = both halves
-      float* xb = xch + 512 - 64 + sp * 16;  // last 64 floats of the exchange area... per sp
-      (void)xb;
-      float* lb = xch + sp * 64;
-      asm volatile("bar.sync %0, 64;" ::"r"(2 + sp));  // both done with the exchange buffers
-      lb[half * 32 + lane] = l_run;
+      float2* xb = xch + sp * 64;
+      xb[grp * 32 + lane] = make_float2(m_run, l_run);
       asm volatile("bar.sync %0, 64;" ::"r"(2 + sp));
-      l_run += lb[(1 - half) * 32 + lane];
-    }
-    const int j = beam, ii = row % g;
-    if (warp_live) {
-      if (p.splits == 1) {
-        __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D + ocol0;
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      const float2 ot = xb[(1 - grp) * 32 + lane];
+      // the other group's last PV must be complete too before O_{1-grp} is read
+      const int olast = ((ntiles - 1 - (1 - grp)) >> 1) * 2 + (1 - grp);
+      if (olast >= 0 && olast < ntiles) {
+        mbar_wait(&pv_done[olast % C::NSB], (uint32_t)(olast / C::NSB) & 1u);
+        tc_fence_after();
+      }
+      const float m0 = grp ? ot.x : m_run, l0 = grp ? ot.y : l_run;
+      const float m1 = grp ? m_run : ot.x, l1 = grp ? l_run : ot.y;
+      const float m = fmaxf(m0, m1);
+      const float a0 = m0 == -INFINITY ? 0.f : ex2(m0 - m), a1 = m1 == -INFINITY ? 0.f : ex2(m1 - m);
+      const float l = l0 * a0 + l1 * a1;
+      const bool has0 = ntiles > 0, has1 = ntiles > 1;  // else O_e is uninitialised TMEM
+      const int j = beam, ii = row % g;
+      constexpr int HD = D / 2;
+      const int c0 = grp * HD;
+      if (!trc) {
+        if (p.splits == 1) {
+          __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
+          const float inv = l > 0.f ? 1.f / l : 0.f;
+          const float f0 = a0 * inv, f1 = a1 * inv;
 #pragma unroll
-        for (int c = 0; c < C::OW; c += 32) {
-          uint32_t o[32];
-          tmem_ld32(tmem + lane_off + C::COL_O + ocol0 + c, o);
-          tmem_wait_ld();
-          if (qvalid) {
-            uint32_t w[16];
+          for (int c = 0; c < HD; c += 16) {
+            uint32_t o0[16], o1[16];
+            tmem_ld16(tmem + lane_off + C::COL_O0 + c0 + c, o0);
+            tmem_ld16(tmem + lane_off + C::COL_O1 + c0 + c, o1);
+            tmem_wait_ld();
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
-              w[k] = pack_bf16(__uint_as_float(o[2 * k]) * inv, __uint_as_float(o[2 * k + 1]) * inv);
+            for (int k = 0; k < 16; ++k) {
+              o0[k] = has0 ? o0[k] : 0u;
+              o1[k] = has1 ? o1[k] : 0u;
+            }
+            if (qvalid) {
+              uint32_t w[8];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              *(int4*)(op + c + 8 * k) = make_int4((int)w[4 * k], (int)w[4 * k + 1], (int)w[4 * k + 2], (int)w[4 * k + 3]);
+              for (int k = 0; k < 8; ++k)
+                w[k] = pack_bf16(__uint_as_float(o0[2 * k]) * f0 + __uint_as_float(o1[2 * k]) * f1,
+                                 __uint_as_float(o0[2 * k + 1]) * f0 + __uint_as_float(o1[2 * k + 1]) * f1);
+              *(int4*)(op + c0 + c) = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+              *(int4*)(op + c0 + c + 8) = make_int4((int)w[4], (int)w[5], (int)w[6], (int)w[7]);
+            }
           }
-        }
-        if (qvalid && half == 0) {
-          if (l_run == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
-          if (p.lse)
-            p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
-                l_run > 0.f ? (m_run + log2f(l_run)) * 0.69314718055994531f : -INFINITY;
-        }
-      } else {
-        float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + row) * (D + 2);
-#pragma unroll
-        for (int c = 0; c < C::OW; c += 32) {
-          uint32_t o[32];
-          tmem_ld32(tmem + lane_off + C::COL_O + ocol0 + c, o);
-          tmem_wait_ld();
-          if (qvalid) {
-#pragma unroll
-            for (int k = 0; k < 32; k += 2)  // rows are (D + 2) floats: 8-byte aligned only
-              *(float2*)(pp + ocol0 + c + k) = make_float2(__uint_as_float(o[k]), __uint_as_float(o[k + 1]));
+          if (qvalid && grp == 0) {
+            if (l == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
+            if (p.lse)
+              p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
+                  l > 0.f ? (m + log2f(l)) * 0.69314718055994531f : -INFINITY;
           }
-        }
-        if (qvalid && half == 0) {
-          pp[D] = m_run;
-          pp[D + 1] = l_run;
+        } else {
+          float* pp = p.part + ((((size_t)r * p.Hkv + h) * p.splits + split) * Qg + row) * (D + 2);
+#pragma unroll
+          for (int c = 0; c < HD; c += 16) {
+            uint32_t o0[16], o1[16];
+            tmem_ld16(tmem + lane_off + C::COL_O0 + c0 + c, o0);
+            tmem_ld16(tmem + lane_off + C::COL_O1 + c0 + c, o1);
+            tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              o0[k] = has0 ? o0[k] : 0u;
+              o1[k] = has1 ? o1[k] : 0u;
+            }
+            if (qvalid) {
+#pragma unroll
+              for (int k = 0; k < 16; k += 2)  // rows are (D + 2) floats: 8-byte aligned only
+                *(float2*)(pp + c0 + c + k) =
+                    make_float2(__uint_as_float(o0[k]) * a0 + __uint_as_float(o1[k]) * a1,
+                                __uint_as_float(o0[k + 1]) * a0 + __uint_as_float(o1[k + 1]) * a1);
+            }
+          }
+          if (qvalid && grp == 0) {
+            pp[D] = m;
+            pp[D + 1] = l;
+          }
         }
       }
     }
   }
+#undef TRC
   // teardown: everyone done with TMEM before the allocating warp frees it
   tc_fence_before();
   __syncthreads();
@@ -439,11 +542,11 @@ struct UKernel {
   const void* fn;
   int smem, threads, occ;
 };
-template <int D, int ST, bool DB, int SW = 2>
+template <int D, int STK, int STV>
 static const UKernel& uk() {
   static const UKernel k = [] {
-    using C = UCfg<D, ST, DB, SW>;
-    auto kern = k_attn_umma<D, ST, DB, SW>;
+    using C = UCfg<D, STK, STV>;
+    auto kern = k_attn_umma<D, STK, STV>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int occ = 0;
@@ -453,40 +556,17 @@ static const UKernel& uk() {
   return k;
 }
 
-// TRIE_UMMA_DB=1 (default): double-buffered S, 4 stages, 1 CTA/SM; 0: single S, 2 stages,
-// 2 CTAs/SM
-static int umma_db() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TRIE_UMMA_DB");
-    v = e ? atoi(e) : 1;  // r05 sweep R=16: DB=1 4.12 TB/s (b=16) vs DB=0 2.85
-  }
-  return v;
-}
 template <int D>
 static const UKernel& select_ud() {
-  // TRIE_UMMA_ST: ring stages (default 4; r07: 2 stages x 2 CTAs/SM starve the ring)
+  // TRIE_UMMA_ST: V ring stages (4, 6 = default, 8; the K ring has 4, 3 with 8 V stages)
   static int st = -1;
   if (st < 0) {
     const char* e = getenv("TRIE_UMMA_ST");
-    st = e ? atoi(e) : 4;
+    st = e ? atoi(e) : 6;
   }
-  static int sw = -1;  // TRIE_UMMA_SW: softmax warps per TMEM sub-partition (1 or 2)
-  if (sw < 0) {
-    const char* e = getenv("TRIE_UMMA_SW");
-    sw = e ? atoi(e) : 2;
-  }
-  if (sw == 1) {
-    if (st >= 4) return uk<D, 4, true, 1>();
-    if (st == 3) return uk<D, 3, true, 1>();
-    return uk<D, 2, true, 1>();
-  }
-  constexpr int SW2 = (D % 64 == 0) ? 2 : 1;  // D = 96: 48 O columns per warp -> SW = 1
-  if (!umma_db()) return uk<D, 2, false, SW2>();
-  if (st >= 5 && UCfg<D, 5, true, SW2>::SMEM <= 227 * 1024) return uk<D, (D <= 128 ? 5 : 4), true, SW2>();
-  if (st >= 4) return uk<D, 4, true, SW2>();
-  if (st == 3) return uk<D, 3, true, SW2>();
-  return uk<D, 2, true, SW2>();
+  if (st >= 8 && UCfg<D, 3, 8>::SMEM <= 227 * 1024) return uk<D, 3, 8>();
+  if (st >= 6) return uk<D, 4, 6>();
+  return uk<D, 4, 4>();
 }
 static const UKernel* select_u(int D) {
   switch (D) {

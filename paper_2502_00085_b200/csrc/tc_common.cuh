@@ -147,7 +147,7 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
                                               const ItemInfo& it, uint8_t* ring, uint64_t* full,
                                               uint64_t* empty, uint64_t* app_done = nullptr,
                                               int first_leaf_slot = INT_MAX, int i_begin = 0,
-                                              int i_end = INT_MAX) {
+                                              int i_end = INT_MAX, uint32_t* trc = nullptr) {
   using RG = Ring<D, STAGES>;
   const int row_base = (r * p.Hkv + h) * p.cap;
   const size_t mbase = (size_t)r * p.cap;
@@ -156,6 +156,7 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
     const int s = i % STAGES;
     const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
     mbar_wait(&empty[s], ph ^ 1u);
+    if (trc && i < 400) trc[i * 12 + 7] = (uint32_t)clock();
     if (!appended && (it.tile0 + i + 1) * TC_TR > first_leaf_slot) {
       // fused RoPE: the consumer wrote this tile's leaf K/V rows (generic proxy) and
       // fenced them for the async proxy before arriving; TMA may read them now
@@ -174,6 +175,7 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
     }
     bulk_load_1d(st + 2 * RG::TILE_BYTES, p.mask + mbase + n0, mdb, &full[s]);
     bulk_load_1d(st + 2 * RG::TILE_BYTES + TC_TR * 4, p.depth + mbase + n0, mdb, &full[s]);
+    if (trc && i < 400) trc[i * 12 + 8] = (uint32_t)clock();
   }
 }
 

@@ -31,6 +31,10 @@ CASES = [
     ("swa-w1", 1, 4, 50, False, 6, 0.5, 4, 1, 64, 1, "f32", True),
     ("b32", 1, 32, 500, False, 10, 0.9, 8, 2, 128, 0, "bf16", True),
     ("b16-g4", 1, 16, 700, False, 8, 0.0, 16, 4, 128, 0, "bf16", True),
+    # tcgen05 path: ragged + window, head_dim 64, and Qg = 48 (a live warp with padding rows)
+    ("b16-swa-ragged", 2, 16, 600, True, 8, 0.5, 16, 4, 128, 200, "bf16", True),
+    ("b32-d64", 1, 32, 300, False, 6, 0.5, 4, 2, 64, 0, "bf16", True),
+    ("b12-g4", 2, 12, 400, True, 6, 0.5, 8, 2, 128, 0, "bf16", True),
     ("b1", 3, 1, 40, True, 5, 0.0, 4, 4, 32, 0, "f32", True),
     ("d256", 1, 2, 70, False, 4, 0.5, 2, 1, 256, 0, "f32", True),
 ]
