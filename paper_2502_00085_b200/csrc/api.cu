@@ -55,7 +55,7 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
   const size_t R = c->n_requests, cap = c->capacity, b = c->beam_width;
-  const size_t chunks = (c->vocab + 4095) / 4096;
+  const size_t chunks = (c->vocab + TRIE_BEAM_CHUNK - 1) / TRIE_BEAM_CHUNK;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     char* p = base ? base + off : nullptr;
@@ -79,6 +79,9 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
   char* cmax = take(R * b * chunks * 4);
   char* csum = take(R * b * chunks * 4);
   char* ctop = take(R * b * chunks * b * 8);
+  char* rlse = take(R * TRIE_MAX_BEAMS * 4);
+  char* rtop = take(R * TRIE_MAX_BEAMS * TRIE_MAX_BEAMS * 8);
+  char* tickets = take(R * (TRIE_MAX_BEAMS + 1) * 4);
   char* sp = take(R * b * 4);
   char* st = take(R * b * 4);
   char* ss = take(R * b * 4);
@@ -101,6 +104,10 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
     h->chunk_max = (float*)cmax;
     h->chunk_sum = (float*)csum;
     h->chunk_top = (uint64_t*)ctop;
+    h->row_lse = (float*)rlse;
+    h->row_top = (uint64_t*)rtop;
+    h->cnt_row = (uint32_t*)tickets;
+    h->cnt_req = (uint32_t*)tickets + R * TRIE_MAX_BEAMS;
     h->sel_parent = (int32_t*)sp;
     h->sel_token = (int32_t*)st;
     h->sel_score = (float*)ss;
@@ -158,6 +165,8 @@ int trie_create(const trie_cfg* cfg, void* workspace, size_t workspace_bytes,
                         (size_t)cfg->n_requests * cfg->max_prompt_len * 4,
                         cudaMemcpyDeviceToDevice, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->status, 0, 4, stream);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(h->cnt_row, 0, (size_t)cfg->n_requests * (TRIE_MAX_BEAMS + 1) * 4, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // prompt_lens_host may be freed
   if (e != cudaSuccess) {
     delete h;
@@ -397,17 +406,8 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
 int trie_beam_step(trie_handle* h, const float* logits, int32_t* sel_parent_beam,
                    int32_t* sel_token, float* new_score, cudaStream_t stream) {
   if (!h || !logits) return trie_set_error(TRIE_EINVAL, "null argument");
-  int rc = trie::launch_beam_step(h, logits, stream);
+  int rc = trie::launch_beam_step(h, logits, sel_parent_beam, sel_token, new_score, stream);
   if (rc) return rc;
-  const size_t n = (size_t)h->cfg.n_requests * h->cfg.beam_width * 4;
-  cudaError_t e = cudaSuccess;
-  if (sel_parent_beam)
-    e = cudaMemcpyAsync(sel_parent_beam, h->sel_parent, n, cudaMemcpyDeviceToDevice, stream);
-  if (e == cudaSuccess && sel_token)
-    e = cudaMemcpyAsync(sel_token, h->sel_token, n, cudaMemcpyDeviceToDevice, stream);
-  if (e == cudaSuccess && new_score)
-    e = cudaMemcpyAsync(new_score, h->sel_score, n, cudaMemcpyDeviceToDevice, stream);
-  if (e != cudaSuccess) return trie_set_error(TRIE_ECUDA, "beam_step copy: %s", cudaGetErrorString(e));
   h->b_live = h->cfg.beam_width;
   h->steps += 1;
   return TRIE_OK;

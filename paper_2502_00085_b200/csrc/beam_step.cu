@@ -2,28 +2,33 @@
 // P:146; Alg. 1 l.6 top-b), then update_trie / update_mask (Alg. 2 l.10-11,
 // P:147-148; §3.3; §3.4 positions P:206).
 //
-// Stage A (k_row_chunk): one CTA per (request, beam row, chunk of CHUNK logits): chunk
-//   max, chunk sum exp(x - max) and the chunk's top-b by (x desc, v asc), from registers
-//   (one HBM pass over the fp32 logits, 16-byte loads).
-// Stage B (k_select_append): one CTA per request: combine chunk (max, sum) into each row's
-//   lse; reduce every row's chunk lists to the row's top-b; score the <= b*b survivors
-//   cs = score_j + (x - lse_j) and take the global top-b in the total order
-//   (cs desc, v asc, j asc) (readings R1, R3); then append (token/parent/depth, leaves,
-//   scores, N) and the bitset update new[n] bit r = old[n] bit j_r.
+// ONE launch, k_beam_step, grid (chunks, R * b_live), 256 threads per CTA:
+//   chunk stage (every CTA): 8192 logits of one (request, beam row) from HBM once
+//     (16-byte streaming loads), chunk max and sum exp(x - max), and the chunk's top-b by
+//     (x desc, v asc).  The top-b is found by THRESHOLD + RANK: each warp bitonic-sorts its
+//     32 lane maxima and takes the b-th (b lanes hold an element >= it, so the chunk has
+//     >= b elements >= T = max over warps); only elements >= T (typically ~b..2b) are
+//     compacted into shared memory and ranked by counting (keys are unique).  If ties
+//     overflow the buffer, the registers are reduced by warp arg-max rounds instead.
+//   row stage (the LAST chunk CTA of a row, atomic ticket): row lse from the chunk
+//     (max, sum) pairs; the row's top-b from the chunk lists (threshold = max over chunks
+//     of each list's b-th key, then rank).
+//   request stage (the LAST row CTA of a request): candidate scores
+//     cs = score_j + (x - lse_j) of the <= b x b survivors, global top-b in the total
+//     order (cs desc, v asc, j asc) (readings R1, R3), then append (token/parent/depth,
+//     leaves, scores, N) and the bitset update new[n] bit r = old[n] bit j_r.
 // Keys: 64-bit, larger = better.  Row stage: ord(x) << 32 | ~v.  Global stage:
 //   ord(cs) << 32 | ~(v * b_live + j).  A row's top-b by x contains that row's top-b by
 //   cs (cs is monotone in x within a row); fp32 rounding of cs can only reorder
 //   candidates whose cs differ by <= 1 ulp -- the near-tie case of the parity protocol.
+// The tickets (cnt_row, cnt_req) are zeroed by trie_create and re-zeroed by the CTA that
+// takes the last ticket, so the kernel is CUDA-graph replayable.
 #include <float.h>
 
 #include "common.cuh"
 #include "handle.h"
 
 namespace trie {
-
-constexpr int BS_A = 256;
-constexpr int ITEMS_A = 16;  // CHUNK = BS_A * ITEMS_A = 4096 logits per CTA
-constexpr int CHUNK = BS_A * ITEMS_A;
 
 __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
   uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
@@ -59,68 +64,108 @@ __device__ __forceinline__ void warp_topk(uint64_t (&key)[ITEMS], int k, uint64_
   }
 }
 
-// ---- Stage A --------------------------------------------------------------------------
-__global__ void __launch_bounds__(BS_A) k_row_chunk(const float* __restrict__ logits, int V,
-                                                    int b_live, int b, int chunks,
-                                                    float* chunk_max, float* chunk_sum,
-                                                    uint64_t* chunk_top) {
-  __shared__ float sm_red[BS_A / 32];
-  __shared__ uint64_t sm_top[BS_A / 32][TRIE_MAX_BEAMS];
-  const int c = blockIdx.x, row = blockIdx.y;  // row = r * b_live + j
-  const float* x = logits + (size_t)row * V;
-  const int v0 = c * CHUNK;
-  float val[ITEMS_A];
-  // coalesced: item i of thread tid is element v0 + i*BS_A + tid
-#pragma unroll
-  for (int i = 0; i < ITEMS_A; ++i) {
-    const int v = v0 + i * BS_A + threadIdx.x;
-    val[i] = v < V ? __ldg(x + v) : -INFINITY;
+// ---- selection helpers ------------------------------------------------------------------
+constexpr int BS = 256;
+constexpr int ITEMS = 32;            // logits per thread
+constexpr int CHUNK = BS * ITEMS;    // 8192 logits per CTA
+static_assert(CHUNK == TRIE_BEAM_CHUNK, "workspace sizing (handle.h)");
+constexpr int CAND_CAP = 512;        // candidate keys buffered by the chunk stage
+
+// Descending top-k of n unique keys (0 = empty) by rank counting: out[rank(x)] = x for
+// rank < k, out[] zero-filled first.  Block-wide; src may be shared or global memory.
+__device__ __forceinline__ void block_rank_topk(const uint64_t* src, int n, int k, uint64_t* out) {
+  for (int i = threadIdx.x; i < k; i += blockDim.x) out[i] = 0ull;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t x = src[i];
+    if (x == 0ull) continue;
+    int rank = 0;
+    for (int j = 0; j < n; ++j) rank += src[j] > x ? 1 : 0;
+    if (rank < k) out[rank] = x;
   }
-  float m = -INFINITY;
+  __syncthreads();
+}
+
+// One value per lane -> the warp's values sorted descending (lane i holds the i-th largest):
+// bitonic sort over shuffles.
+__device__ __forceinline__ float warp_sort_desc(float v) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int i = 0; i < ITEMS_A; ++i) m = fmaxf(m, val[i]);
-  m = warp_max(m);
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const float o = __shfl_xor_sync(0xffffffffu, v, stride);
+      const bool desc = (lane & size) == 0;
+      const bool lower = (lane & stride) == 0;
+      v = (lower == desc) ? fmaxf(v, o) : fminf(v, o);
+    }
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_sort_desc_u64(uint64_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint64_t o = shfl_xor_u64(v, stride);
+      const bool desc = (lane & size) == 0;
+      const bool lower = (lane & stride) == 0;
+      v = (lower == desc) ? (o > v ? o : v) : (o < v ? o : v);
+    }
+  }
+  return v;
+}
+
+// Top-32 of two descending 32-lists (lane i holds the i-th entry; 0 pads): C[i] =
+// max(A[i], B[31 - i]) holds the top 32 of A u B and is bitonic, so one bitonic merge
+// (5 shuffle stages) sorts it descending.
+__device__ __forceinline__ uint64_t warp_merge_top32(uint64_t a, uint64_t b) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t br = shfl_u64(b, 31 - lane);
+  uint64_t c = a > br ? a : br;
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    const uint64_t o = shfl_xor_u64(c, stride);
+    c = ((lane & stride) == 0) ? (o > c ? o : c) : (o < c ? o : c);
+  }
+  return c;
+}
+
+// Every warp holds a descending 32-list in `acc`; merge the 8 lists pairwise (3 levels)
+// through `buf` [8][32]; the block's top-32 ends in buf[0][0..32).
+__device__ __forceinline__ void block_merge_tree(uint64_t acc, uint64_t (*buf)[32]) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) sm_red[w] = m;
+  buf[w][lane] = acc;
   __syncthreads();
-  m = sm_red[0];
 #pragma unroll
-  for (int i = 1; i < BS_A / 32; ++i) m = fmaxf(m, sm_red[i]);
-  __syncthreads();
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < ITEMS_A; ++i) s += (val[i] == -INFINITY) ? 0.f : expf(val[i] - m);
-  s = warp_sum(s);
-  if (lane == 0) sm_red[w] = s;
-  // top-b keys of this chunk
-  uint64_t key[ITEMS_A];
-#pragma unroll
-  for (int i = 0; i < ITEMS_A; ++i) {
-    const int v = v0 + i * BS_A + threadIdx.x;
-    key[i] = v < V ? ((uint64_t)f2ord(val[i]) << 32) | (uint32_t)(~(uint32_t)v) : 0ull;
+  for (int n = 4; n >= 1; n >>= 1) {
+    uint64_t m = 0ull;
+    if (w < n) m = warp_merge_top32(buf[w][lane], buf[w + n][lane]);
+    __syncthreads();
+    if (w < n) buf[w][lane] = m;
+    __syncthreads();
   }
-  const int k = min(b, CHUNK);
-  warp_topk<ITEMS_A>(key, k, sm_top[w]);
-  __syncthreads();
-  const size_t o = (size_t)row * chunks + c;
-  if (w == 0) {
-    // merge the 8 warp lists (8*k <= 256 keys, 8 per lane)
-    uint64_t kk[8];
+}
+
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// val[i] for a runtime i without local-memory indexing
+template <int N>
+__device__ __forceinline__ float sel_item(const float (&val)[N], int i) {
+  float x = val[0];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int idx = i * 32 + lane;
-      const int ww = idx / TRIE_MAX_BEAMS, pos = idx % TRIE_MAX_BEAMS;
-      kk[i] = (ww < BS_A / 32 && pos < k) ? sm_top[ww][pos] : 0ull;
-    }
-    uint64_t* dst = chunk_top + o * b;
-    warp_topk<8>(kk, k, dst);
-    if (lane == 0) {
-      float tot = 0.f;
-      for (int i = 0; i < BS_A / 32; ++i) tot += sm_red[i];
-      chunk_max[o] = m;
-      chunk_sum[o] = tot;
-    }
-  }
+  for (int u = 1; u < N; ++u) x = i == u ? val[u] : x;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t row_key(float x, int v) {
+  return ((uint64_t)f2ord(x) << 32) | (uint32_t)(~(uint32_t)v);
 }
 
 // ---- append (Alg. 2 l.10-11) -----------------------------------------------------------
@@ -185,112 +230,286 @@ __global__ void k_append(const int32_t* par, const int32_t* tok, const float* sc
              tlen, cap, status);
 }
 
-// ---- Stage B ---------------------------------------------------------------------------
-constexpr int BS_B = 256;
-__global__ void __launch_bounds__(BS_B) k_select_append(
-    const float* chunk_max, const float* chunk_sum, const uint64_t* chunk_top, int b_live,
-    int b, int chunks, int32_t* token, int32_t* parent, int32_t* depth, uint32_t* mask,
-    int32_t* leaf, float* score, int32_t* nn, int32_t* nkv, const int32_t* tlen, int cap,
-    uint32_t* status, int32_t* out_par, int32_t* out_tok, float* out_sc) {
-  __shared__ float sm_lse[TRIE_MAX_BEAMS];
-  __shared__ uint64_t sm_row[TRIE_MAX_BEAMS][TRIE_MAX_BEAMS];  // each row's top-b by x
-  __shared__ uint64_t sm_sel[TRIE_MAX_BEAMS];
-  __shared__ int sp[TRIE_MAX_BEAMS], st[TRIE_MAX_BEAMS];
-  __shared__ float ss[TRIE_MAX_BEAMS];
-  const int r = blockIdx.x;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int k = b;  // candidates needed per row (b <= V guaranteed by the host)
-  // (1) per row: lse from chunk (max, sum); the row's top-k from its chunk lists
-  for (int j = w; j < b_live; j += BS_B / 32) {
-    const size_t rowi = (size_t)r * b_live + j;
-    float M = -INFINITY;
-    for (int c = lane; c < chunks; c += 32) M = fmaxf(M, chunk_max[rowi * chunks + c]);
-    M = warp_max(M);
-    float S = 0.f;
-    for (int c = lane; c < chunks; c += 32) {
-      const float cm = chunk_max[rowi * chunks + c];
-      S += chunk_sum[rowi * chunks + c] * expf(cm - M);
-    }
-    S = warp_sum(S);
-    if (lane == 0) sm_lse[j] = M + logf(S);
-    // chunks * k keys; process in slices of 32*ITEMS and keep a running top-k
-    constexpr int IT = 8;
-    uint64_t best[IT];  // running top-k held in the first k of a 32*IT pool
-    const int total = chunks * k;
-    const uint64_t* src = chunk_top + rowi * chunks * b;
-    // pool = running list (k <= 32, lane-distributed at item 0) + next slice
-    uint64_t run = 0ull;  // lane l holds running[l] (l < k)
-    for (int s0 = 0; s0 < total; s0 += 32 * (IT - 1)) {
-      best[0] = run;
-#pragma unroll
-      for (int i = 1; i < IT; ++i) {
-        const int idx = s0 + (i - 1) * 32 + lane;
-        best[i] = 0ull;
-        if (idx < total) {
-          const int c = idx / k, pos = idx % k;
-          best[i] = src[(size_t)c * b + pos];
-        }
-      }
-      uint64_t* dst = &sm_row[j][0];
-      warp_topk<IT>(best, k, dst);
-      __syncwarp();
-      run = lane < k ? dst[lane] : 0ull;
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  // (2) global: b_live * k candidates keyed by (cs, ~(v*b_live + j))
-  {
-    constexpr int IT = 32;  // b_live*k <= 1024 = 32 lanes * 32 items, handled by warp 0
-    if (w == 0) {
-      uint64_t key[IT];
-#pragma unroll
-      for (int i = 0; i < IT; ++i) {
-        const int idx = i * 32 + lane;
-        key[i] = 0ull;
-        const int j = idx / k, pos = idx % k;
-        if (j < b_live) {
-          const uint64_t rk = sm_row[j][pos];
-          if (rk != 0ull) {
-            const float x = ord2f((uint32_t)(rk >> 32));
-            const uint32_t v = ~(uint32_t)rk;
-            const float cs = score[r * TRIE_MAX_BEAMS + j] + (x - sm_lse[j]);
-            key[i] = ((uint64_t)f2ord(cs) << 32) | (uint32_t)(~(v * (uint32_t)b_live + j));
-          }
-        }
-      }
-      warp_topk<IT>(key, b, sm_sel);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < b) {
-    const uint64_t kk = sm_sel[threadIdx.x];
-    const uint32_t id = ~(uint32_t)kk;
-    sp[threadIdx.x] = (int)(id % (uint32_t)b_live);
-    st[threadIdx.x] = (int)(id / (uint32_t)b_live);
-    ss[threadIdx.x] = ord2f((uint32_t)(kk >> 32));
-    if (out_par) out_par[r * b + threadIdx.x] = sp[threadIdx.x];
-    if (out_tok) out_tok[r * b + threadIdx.x] = st[threadIdx.x];
-    if (out_sc) out_sc[r * b + threadIdx.x] = ss[threadIdx.x];
-  }
-  __syncthreads();
-  append_sel(r, b, b_live, sp, st, ss, token, parent, depth, mask, leaf, score, nn, nkv, tlen,
-             cap, status);
+// ---- the fused beam step ----------------------------------------------------------------
+struct BeamStepArgs {
+  const float* logits;
+  int V, b_live, b, chunks;
+  float* chunk_max;
+  float* chunk_sum;
+  uint64_t* chunk_top;   // [R * b_live][chunks][b]
+  float* row_lse;        // [R][32]
+  uint64_t* row_top;     // [R][32][32]
+  uint32_t* cnt_row;     // [R * 32]
+  uint32_t* cnt_req;     // [R]
+  int32_t *token, *parent, *depth;
+  uint32_t* mask;
+  int32_t* leaf;
+  float* score;
+  int32_t *nn, *nkv;
+  const int32_t* tlen;
+  int cap;
+  uint32_t* status;
+  int32_t *sel_par, *sel_tok;
+  float* sel_sc;
+  int32_t *out_par, *out_tok;
+  float* out_sc;
+};
+
+// element index of item i of this thread within the row
+template <bool VEC>
+__device__ __forceinline__ int item_v(int v0, int i) {
+  return VEC ? v0 + 4 * ((i >> 2) * BS + (int)threadIdx.x) + (i & 3) : v0 + i * BS + (int)threadIdx.x;
 }
 
-int launch_beam_step(trie_handle* h, const float* logits, cudaStream_t s) {
+template <bool VEC>
+__global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
+  __shared__ float sm_red[BS / 32];
+  __shared__ float sm_ta[BS / 32], sm_tb[BS / 32];
+  __shared__ uint64_t sm_cand[CAND_CAP];
+  __shared__ uint64_t sm_wtop[BS / 32][TRIE_MAX_BEAMS];
+  __shared__ uint64_t sm_mrg[BS / 32][32];
+  __shared__ float sm_lse[TRIE_MAX_BEAMS];
+  __shared__ int sm_n, sm_last;
+  __shared__ int sp[TRIE_MAX_BEAMS], st[TRIE_MAX_BEAMS];
+  __shared__ float ss[TRIE_MAX_BEAMS];
+  const int c = blockIdx.x, row = blockIdx.y;
+  const int r = row / a.b_live, j_row = row % a.b_live;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int V = a.V, k = a.b;  // candidates kept per chunk / row (b <= V, b <= 32)
+  const float* x = a.logits + (size_t)row * V;
+  const int v0 = c * CHUNK;
+
+  // ---- chunk stage: one HBM pass ------------------------------------------------------
+  float val[ITEMS];
+  if (VEC) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll
+    for (int q = 0; q < ITEMS / 4; ++q) {
+      const int e = item_v<true>(v0, 4 * q);
+      float4 f = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      if (e < V) f = __ldcs(x4 + (e >> 2));  // V % 4 == 0: all four valid
+      val[4 * q + 0] = f.x; val[4 * q + 1] = f.y; val[4 * q + 2] = f.z; val[4 * q + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = item_v<false>(v0, i);
+      val[i] = e < V ? __ldcs(x + e) : -INFINITY;
+    }
+  }
+  if (threadIdx.x == 0) sm_n = 0;
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) m = fmaxf(m, val[i]);  // padding items are -inf
+  // threshold T (at least k elements of the chunk are >= T), from the warps' sorted lane
+  // maxima: (a) the k-th largest lane maximum of any warp; (b) the minimum over the 8
+  // warps of each warp's ceil(k/8)-th largest (8 * ceil(k/8) >= k elements).  T = max.
+  const float srt = warp_sort_desc(m);
+  const float ta = __shfl_sync(0xffffffffu, srt, k - 1);
+  const float tb = __shfl_sync(0xffffffffu, srt, (k + BS / 32 - 1) / (BS / 32) - 1);
+  m = __shfl_sync(0xffffffffu, srt, 0);
+  if (lane == 0) { sm_red[w] = m; sm_ta[w] = ta; sm_tb[w] = tb; }
+  __syncthreads();
+  m = sm_red[0];
+  float T = sm_ta[0], Tb = sm_tb[0];
+#pragma unroll
+  for (int i = 1; i < BS / 32; ++i) {
+    m = fmaxf(m, sm_red[i]);
+    T = fmaxf(T, sm_ta[i]);
+    Tb = fminf(Tb, sm_tb[i]);
+  }
+  T = fmaxf(T, Tb);
+  __syncthreads();
+  // sum exp(x - m) = sum 2^(x log2e - m log2e): one FFMA + one MUFU.EX2 per logit
+  // (ex2.approx: ~2 ulp, far inside the 1e-4 score tolerance); exp2(-inf) = 0 for padding
+  float s = 0.f;
+  const float ml2 = m == -INFINITY ? 0.f : m * 1.4426950408889634f;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) s += ex2_approx(fmaf(val[i], 1.4426950408889634f, -ml2));
+  s = warp_sum(s);
+  if (lane == 0) sm_red[w] = s;
+  // candidates: one compare per logit into a bit set; the (rare) set bits are pushed
+  uint32_t bits = 0u;
+#pragma unroll
+  for (int i = 0; i < ITEMS; ++i) bits |= (val[i] >= T ? 1u : 0u) << i;
+  if (T == -INFINITY) {  // too few finite logits: drop the -inf padding items
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (item_v<VEC>(v0, i) >= V) bits &= ~(1u << i);
+  }
+  while (bits) {
+    const int i = __ffs(bits) - 1;
+    bits &= bits - 1;
+    const int pos = atomicAdd(&sm_n, 1);
+    if (pos < CAND_CAP) sm_cand[pos] = row_key(sel_item(val, i), item_v<VEC>(v0, i));
+  }
+  __syncthreads();
+  const size_t o = (size_t)row * a.chunks + c;
+  uint64_t* ctop = a.chunk_top + o * a.b;
+  const int n_cand = sm_n;
+  if (n_cand <= CAND_CAP) {
+    block_rank_topk(sm_cand, n_cand, k, ctop);
+  } else {  // ties overflowed the buffer: warp arg-max rounds over the registers
+    // k rounds of warp arg-max; keys are rebuilt from val[] (a taken-bit per item)
+    uint32_t taken = 0u;
+    for (int q = 0; q < k; ++q) {
+      uint64_t best = 0ull;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i) {
+        const int v = item_v<VEC>(v0, i);
+        const uint64_t key = (v < V && !((taken >> i) & 1u)) ? row_key(val[i], v) : 0ull;
+        best = key > best ? key : best;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const uint64_t y = shfl_xor_u64(best, off);
+        best = y > best ? y : best;
+      }
+      if (lane == 0) sm_wtop[w][q] = best;
+#pragma unroll
+      for (int i = 0; i < ITEMS; ++i)
+        if (best != 0ull && item_v<VEC>(v0, i) < V && row_key(val[i], item_v<VEC>(v0, i)) == best)
+          taken |= 1u << i;
+    }
+    __syncthreads();
+    if (w == 0) {
+      uint64_t kk[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int idx = i * 32 + lane;
+        const int ww = idx / TRIE_MAX_BEAMS, pos = idx % TRIE_MAX_BEAMS;
+        kk[i] = (ww < BS / 32 && pos < k) ? sm_wtop[ww][pos] : 0ull;
+      }
+      warp_topk<8>(kk, k, ctop);
+    }
+  }
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int i = 0; i < BS / 32; ++i) tot += sm_red[i];
+    a.chunk_max[o] = m;
+    a.chunk_sum[o] = tot;
+  }
+  // ---- ticket: the last chunk CTA of this row continues --------------------------------
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // the CTA's writes (ordered by the barrier) before the ticket
+    sm_last = atomicAdd(&a.cnt_row[row], 1u) == (unsigned)(a.chunks - 1);
+  }
+  __syncthreads();
+  if (!sm_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) a.cnt_row[row] = 0u;
+
+  // ---- row stage: lse and the row's top-b ------------------------------------------------
+  const size_t rowi = (size_t)row * a.chunks;
+  if (w == 0) {
+    float M = -INFINITY;
+    for (int cc = lane; cc < a.chunks; cc += 32) M = fmaxf(M, __ldcg(a.chunk_max + rowi + cc));
+    M = warp_max(M);
+    float S = 0.f;
+    for (int cc = lane; cc < a.chunks; cc += 32)
+      S += __ldcg(a.chunk_sum + rowi + cc) * expf(__ldcg(a.chunk_max + rowi + cc) - M);
+    S = warp_sum(S);
+    if (lane == 0) a.row_lse[r * TRIE_MAX_BEAMS + j_row] = M + logf(S);
+  }
+  // the chunk lists (sorted descending, zero padded) merged: each warp folds chunks
+  // w, w + 8, ... into a running top-32, then a 3-level tree over the warps
+  const uint64_t* lists = a.chunk_top + rowi * a.b;
+  {
+    uint64_t acc = 0ull;
+    for (int cc = w; cc < a.chunks; cc += BS / 32) {
+      const uint64_t x = lane < k ? __ldcg(lists + (size_t)cc * a.b + lane) : 0ull;
+      acc = warp_merge_top32(acc, x);
+    }
+    block_merge_tree(acc, sm_mrg);
+  }
+  uint64_t* rtop = a.row_top + ((size_t)r * TRIE_MAX_BEAMS + j_row) * TRIE_MAX_BEAMS;
+  if (threadIdx.x < k) rtop[threadIdx.x] = sm_mrg[0][threadIdx.x];
+  // ---- ticket: the last row CTA of this request continues --------------------------------
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    sm_last = atomicAdd(&a.cnt_req[r], 1u) == (unsigned)(a.b_live - 1);
+  }
+  __syncthreads();
+  if (!sm_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) a.cnt_req[r] = 0u;
+
+  // ---- request stage: global top-b over b_live x k survivors ------------------------------
+  const int b_live = a.b_live;
+  if (threadIdx.x < b_live) sm_lse[threadIdx.x] = __ldcg(a.row_lse + r * TRIE_MAX_BEAMS + threadIdx.x);
+  __syncthreads();
+  // each warp takes rows w, w + 8, ...: lane = position in the row's list.  The row list
+  // is in (x desc, v asc) order, which is (cs desc) order up to fp32 ties of cs; re-sort
+  // only if a tie left it out of global-key order, then merge (as in the row stage)
+  {
+    uint64_t acc = 0ull;
+    for (int j = w; j < b_live; j += BS / 32) {
+      uint64_t gk = 0ull;
+      if (lane < k) {
+        const uint64_t rk = __ldcg(a.row_top + ((size_t)r * TRIE_MAX_BEAMS + j) * TRIE_MAX_BEAMS + lane);
+        if (rk != 0ull) {
+          const float xv = ord2f((uint32_t)(rk >> 32));
+          const uint32_t v = ~(uint32_t)rk;
+          const float cs = a.score[r * TRIE_MAX_BEAMS + j] + (xv - sm_lse[j]);
+          gk = ((uint64_t)f2ord(cs) << 32) | (uint32_t)(~(v * (uint32_t)b_live + j));
+        }
+      }
+      const uint64_t nxt = shfl_u64(gk, (lane + 1) & 31);
+      if (!__all_sync(0xffffffffu, lane == 31 || gk >= nxt)) gk = warp_sort_desc_u64(gk);
+      acc = warp_merge_top32(acc, gk);
+    }
+    block_merge_tree(acc, sm_mrg);
+  }
+  const uint64_t* sel = sm_mrg[0];
+  if (threadIdx.x < a.b) {
+    const uint64_t kk = sel[threadIdx.x];
+    const uint32_t id = ~(uint32_t)kk;
+    const int q = threadIdx.x;
+    sp[q] = (int)(id % (uint32_t)b_live);
+    st[q] = (int)(id / (uint32_t)b_live);
+    ss[q] = ord2f((uint32_t)(kk >> 32));
+    const int o2 = r * a.b + q;
+    a.sel_par[o2] = sp[q]; a.sel_tok[o2] = st[q]; a.sel_sc[o2] = ss[q];
+    if (a.out_par) a.out_par[o2] = sp[q];
+    if (a.out_tok) a.out_tok[o2] = st[q];
+    if (a.out_sc) a.out_sc[o2] = ss[q];
+  }
+  __syncthreads();
+  append_sel(r, a.b, b_live, sp, st, ss, a.token, a.parent, a.depth, a.mask, a.leaf, a.score,
+             a.nn, a.nkv, a.tlen, a.cap, a.status);
+}
+
+int launch_beam_step(trie_handle* h, const float* logits, int32_t* out_par, int32_t* out_tok,
+                     float* out_sc, cudaStream_t s) {
   const trie_cfg& c = h->cfg;
-  const int chunks = (c.vocab + CHUNK - 1) / CHUNK;
-  dim3 ga(chunks, c.n_requests * h->b_live);
-  k_row_chunk<<<ga, BS_A, 0, s>>>(logits, c.vocab, h->b_live, c.beam_width, chunks,
-                                  h->chunk_max, h->chunk_sum, h->chunk_top);
-  int rc = trie_check_launch("k_row_chunk");
-  if (rc) return rc;
-  k_select_append<<<c.n_requests, BS_B, 0, s>>>(
-      h->chunk_max, h->chunk_sum, h->chunk_top, h->b_live, c.beam_width, chunks, h->token,
-      h->parent, h->depth, h->mask, h->leaf, h->score, h->n_nodes, h->n_kv, h->tlen, c.capacity,
-      h->status, h->sel_parent, h->sel_token, h->sel_score);
-  return trie_check_launch("k_select_append");
+  BeamStepArgs a;
+  a.logits = logits;
+  a.V = c.vocab;
+  a.b_live = h->b_live;
+  a.b = c.beam_width;
+  a.chunks = (c.vocab + CHUNK - 1) / CHUNK;
+  const bool vec = (c.vocab % 4 == 0) && ((uintptr_t)logits % 16 == 0);
+  a.chunk_max = h->chunk_max;
+  a.chunk_sum = h->chunk_sum;
+  a.chunk_top = h->chunk_top;
+  a.row_lse = h->row_lse;
+  a.row_top = h->row_top;
+  a.cnt_row = h->cnt_row;
+  a.cnt_req = h->cnt_req;
+  a.token = h->token; a.parent = h->parent; a.depth = h->depth; a.mask = h->mask;
+  a.leaf = h->leaf; a.score = h->score; a.nn = h->n_nodes; a.nkv = h->n_kv; a.tlen = h->tlen;
+  a.cap = c.capacity;
+  a.status = h->status;
+  a.sel_par = h->sel_parent; a.sel_tok = h->sel_token; a.sel_sc = h->sel_score;
+  a.out_par = out_par; a.out_tok = out_tok; a.out_sc = out_sc;
+  dim3 grid(a.chunks, c.n_requests * h->b_live);
+  if (vec)
+    k_beam_step<true><<<grid, BS, 0, s>>>(a);
+  else
+    k_beam_step<false><<<grid, BS, 0, s>>>(a);
+  return trie_check_launch("k_beam_step");
 }
 
 int launch_append(trie_handle* h, const int32_t* par, const int32_t* tok, const float* sc,

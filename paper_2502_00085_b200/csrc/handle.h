@@ -31,6 +31,10 @@ struct trie_handle {
   float* chunk_max = nullptr;     // [R][b][chunks]
   float* chunk_sum = nullptr;     // [R][b][chunks]
   uint64_t* chunk_top = nullptr;  // [R][b][chunks][b]  key = ord(x) << 32 | ~v
+  float* row_lse = nullptr;       // [R][32]
+  uint64_t* row_top = nullptr;    // [R][32][32] each row's top-b keys
+  uint32_t* cnt_row = nullptr;    // [R][32] beam-step tickets (zeroed at create)
+  uint32_t* cnt_req = nullptr;    // [R]
   int32_t* sel_parent = nullptr;  // [R][b]
   int32_t* sel_token = nullptr;   // [R][b]
   float* sel_score = nullptr;     // [R][b]
@@ -39,12 +43,14 @@ struct trie_handle {
   float rope_tab_theta = 0.f;
   int32_t rope_tab_blive = 0;
   int32_t chunks = 1;
-  int32_t chunk_len = 4096;
   // host-tracked state
   int32_t b_live = 1;
   int32_t steps = 0;
   std::vector<int32_t> host_tlen;
 };
+
+// logits per beam-step chunk CTA (beam_step.cu)
+constexpr int TRIE_BEAM_CHUNK = 8192;
 
 // carve the workspace; with h == nullptr only computes the size
 size_t trie_layout(const trie_cfg* cfg, trie_handle* h, char* base);
@@ -54,7 +60,8 @@ namespace trie {
 int launch_init(trie_handle* h, cudaStream_t s);
 int launch_append(trie_handle* h, const int32_t* par, const int32_t* tok, const float* sc,
                   cudaStream_t s);
-int launch_beam_step(trie_handle* h, const float* logits, cudaStream_t s);
+int launch_beam_step(trie_handle* h, const float* logits, int32_t* out_par, int32_t* out_tok,
+                     float* out_sc, cudaStream_t s);
 int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t s);
 int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, void* kpool,
                        void* vpool, float theta, cudaStream_t s);
