@@ -4,19 +4,21 @@
 //
 // ONE launch, k_beam_step, grid (chunks, R * b_live), 256 threads per CTA:
 //   chunk stage (every CTA): 8192 logits of one (request, beam row) from HBM once
-//     (16-byte streaming loads), chunk max and sum exp(x - max), and the chunk's top-b by
-//     (x desc, v asc).  The top-b is found by THRESHOLD + RANK: each warp bitonic-sorts its
-//     32 lane maxima and takes the b-th (b lanes hold an element >= it, so the chunk has
-//     >= b elements >= T = max over warps); only elements >= T (typically ~b..2b) are
-//     compacted into shared memory and ranked by counting (keys are unique).  If ties
-//     overflow the buffer, the registers are reduced by warp arg-max rounds instead.
-//   row stage (the LAST chunk CTA of a row, atomic ticket): row lse from the chunk
-//     (max, sum) pairs; the row's top-b from the chunk lists (threshold = max over chunks
-//     of each list's b-th key, then rank).
+//     (16-byte streaming loads, 32 per thread in registers), chunk max and sum
+//     exp(x - max) (packed FFMA2 + MUFU.EX2), and the chunk's top-b by (x desc, v asc).
+//     The top-b is THRESHOLD + SORT: every warp has ceil(b/8) lanes whose maximum is
+//     >= its ceil(b/8)-th largest lane maximum (redux.sync rounds), so the chunk has >= b
+//     elements >= T = the minimum of that over the 8 warps; only elements >= T (a few x b)
+//     are pushed to shared memory and sorted (one warp bitonic sort when <= 32, rank
+//     counting up to 512).  If ties overflow the buffer, warp arg-max rounds instead.
+//   row stage (the LAST chunk CTA of a row, acq_rel atomic ticket): row lse from the
+//     chunk (max, sum) pairs; the row's top-b by a bitonic merge tree of the chunk lists
+//     (top-32 of two sorted lists = one bitonic merge of max(A[i], B[31-i])).
 //   request stage (the LAST row CTA of a request): candidate scores
-//     cs = score_j + (x - lse_j) of the <= b x b survivors, global top-b in the total
-//     order (cs desc, v asc, j asc) (readings R1, R3), then append (token/parent/depth,
-//     leaves, scores, N) and the bitset update new[n] bit r = old[n] bit j_r.
+//     cs = score_j + (x - lse_j) of the b_live x b survivors, global top-b in the total
+//     order (cs desc, v asc, j asc) (readings R1, R3) by the same merge tree, then append
+//     (token/parent/depth, leaves, scores, N) and the bitset update
+//     new[n] bit r = old[n] bit j_r.
 // Keys: 64-bit, larger = better.  Row stage: ord(x) << 32 | ~v.  Global stage:
 //   ord(cs) << 32 | ~(v * b_live + j).  A row's top-b by x contains that row's top-b by
 //   cs (cs is monotone in x within a row); fp32 rounding of cs can only reorder
@@ -149,19 +151,34 @@ __device__ __forceinline__ void block_merge_tree(uint64_t acc, uint64_t (*buf)[3
 }
 
 
+// ticket counter increment with release + acquire semantics at gpu scope: the barrier
+// before it orders the CTA's writes; the barrier after it publishes the acquire
+__device__ __forceinline__ uint32_t ticket_acq_rel(uint32_t* p) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
-// val[i] for a runtime i without local-memory indexing
-template <int N>
-__device__ __forceinline__ float sel_item(const float (&val)[N], int i) {
-  float x = val[0];
-#pragma unroll
-  for (int u = 1; u < N; ++u) x = i == u ? val[u] : x;
-  return x;
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return r;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return r;
 }
 
 __device__ __forceinline__ uint64_t row_key(float x, int v) {
@@ -261,10 +278,16 @@ __device__ __forceinline__ int item_v(int v0, int i) {
   return VEC ? v0 + 4 * ((i >> 2) * BS + (int)threadIdx.x) + (i & 3) : v0 + i * BS + (int)threadIdx.x;
 }
 
+// One work item = one chunk of one (request, beam) row, then (ticket) its row stage, then
+// (ticket) its request stage.  val[] holds the chunk's logits (-inf padding); with sval
+// != nullptr the same values are also in shared memory in load order (element v0 + e at
+// sval[e]), which the candidate push reads by index.
 template <bool VEC>
-__global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
-  __shared__ float sm_red[BS / 32];
-  __shared__ float sm_ta[BS / 32], sm_tb[BS / 32];
+__device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
+                                          const float (&val)[ITEMS], const float* sval) {
+  __shared__ uint32_t sm_red[BS / 32], sm_tb[BS / 32];
+  __shared__ float sm_sum[BS / 32];
+  __shared__ __align__(16) float sm_stage[BS * ITEMS];
   __shared__ uint64_t sm_cand[CAND_CAP];
   __shared__ uint64_t sm_wtop[BS / 32][TRIE_MAX_BEAMS];
   __shared__ uint64_t sm_mrg[BS / 32][32];
@@ -272,63 +295,54 @@ __global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
   __shared__ int sm_n, sm_last;
   __shared__ int sp[TRIE_MAX_BEAMS], st[TRIE_MAX_BEAMS];
   __shared__ float ss[TRIE_MAX_BEAMS];
-  const int c = blockIdx.x, row = blockIdx.y;
   const int r = row / a.b_live, j_row = row % a.b_live;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int V = a.V, k = a.b;  // candidates kept per chunk / row (b <= V, b <= 32)
-  const float* x = a.logits + (size_t)row * V;
   const int v0 = c * CHUNK;
 
-  // ---- chunk stage: one HBM pass ------------------------------------------------------
-  float val[ITEMS];
-  if (VEC) {
-    const float4* x4 = reinterpret_cast<const float4*>(x);
-#pragma unroll
-    for (int q = 0; q < ITEMS / 4; ++q) {
-      const int e = item_v<true>(v0, 4 * q);
-      float4 f = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      if (e < V) f = __ldcs(x4 + (e >> 2));  // V % 4 == 0: all four valid
-      val[4 * q + 0] = f.x; val[4 * q + 1] = f.y; val[4 * q + 2] = f.z; val[4 * q + 3] = f.w;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-      const int e = item_v<false>(v0, i);
-      val[i] = e < V ? __ldcs(x + e) : -INFINITY;
-    }
-  }
+  // ---- chunk stage ----------------------------------------------------------------------
   if (threadIdx.x == 0) sm_n = 0;
   float m = -INFINITY;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) m = fmaxf(m, val[i]);  // padding items are -inf
-  // threshold T (at least k elements of the chunk are >= T), from the warps' sorted lane
-  // maxima: (a) the k-th largest lane maximum of any warp; (b) the minimum over the 8
-  // warps of each warp's ceil(k/8)-th largest (8 * ceil(k/8) >= k elements).  T = max.
-  const float srt = warp_sort_desc(m);
-  const float ta = __shfl_sync(0xffffffffu, srt, k - 1);
-  const float tb = __shfl_sync(0xffffffffu, srt, (k + BS / 32 - 1) / (BS / 32) - 1);
-  m = __shfl_sync(0xffffffffu, srt, 0);
-  if (lane == 0) { sm_red[w] = m; sm_ta[w] = ta; sm_tb[w] = tb; }
+  // threshold T with >= k elements of the chunk >= T: every warp has >= mk = ceil(k/8)
+  // lanes whose maximum is >= its mk-th largest lane maximum tb_w (redux rounds, one lane
+  // excluded per round), so T = min over the 8 warps of tb_w
+  const uint32_t mkey = f2ord(m);
+  const uint32_t wmax = __reduce_max_sync(0xffffffffu, mkey);
+  uint32_t tb = wmax;
+  {
+    uint32_t kk = mkey;
+    for (int q = 1; q < (k + BS / 32 - 1) / (BS / 32); ++q) {
+      const uint32_t who = __ballot_sync(0xffffffffu, kk == tb);
+      if (lane == __ffs(who) - 1) kk = 0u;
+      tb = __reduce_max_sync(0xffffffffu, kk);
+    }
+  }
+  if (lane == 0) { sm_red[w] = wmax; sm_tb[w] = tb; }
   __syncthreads();
-  m = sm_red[0];
-  float T = sm_ta[0], Tb = sm_tb[0];
+  uint32_t mo = sm_red[0], to = sm_tb[0];
 #pragma unroll
   for (int i = 1; i < BS / 32; ++i) {
-    m = fmaxf(m, sm_red[i]);
-    T = fmaxf(T, sm_ta[i]);
-    Tb = fminf(Tb, sm_tb[i]);
+    mo = max(mo, sm_red[i]);
+    to = min(to, sm_tb[i]);
   }
-  T = fmaxf(T, Tb);
-  __syncthreads();
-  // sum exp(x - m) = sum 2^(x log2e - m log2e): one FFMA + one MUFU.EX2 per logit
-  // (ex2.approx: ~2 ulp, far inside the 1e-4 score tolerance); exp2(-inf) = 0 for padding
-  float s = 0.f;
-  const float ml2 = m == -INFINITY ? 0.f : m * 1.4426950408889634f;
+  m = ord2f(mo);
+  const float T = ord2f(to);
+  // sum exp(x - m) = sum 2^(x log2e - m log2e): packed FFMA2 / FADD2 + one MUFU.EX2 per
+  // logit (ex2.approx: ~2 ulp, far inside the 1e-4 score tolerance); padding -> 2^-inf = 0
+  const float l2e = 1.4426950408889634f;
+  const float nml = m == -INFINITY ? 0.f : -m * l2e;
+  float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int i = 0; i < ITEMS; ++i) s += ex2_approx(fmaf(val[i], 1.4426950408889634f, -ml2));
-  s = warp_sum(s);
-  if (lane == 0) sm_red[w] = s;
-  // candidates: one compare per logit into a bit set; the (rare) set bits are pushed
+  for (int i = 0; i < ITEMS; i += 2) {
+    const float2 y = ffma2(make_float2(val[i], val[i + 1]), make_float2(l2e, l2e), make_float2(nml, nml));
+    acc = fadd2(acc, make_float2(ex2_approx(y.x), ex2_approx(y.y)));
+  }
+  float s = warp_sum(acc.x + acc.y);
+  if (lane == 0) sm_sum[w] = s;
+  // candidates: one compare per logit into a bit set; lanes with set bits stage their
+  // values in shared memory and push (value, index) keys
   uint32_t bits = 0u;
 #pragma unroll
   for (int i = 0; i < ITEMS; ++i) bits |= (val[i] >= T ? 1u : 0u) << i;
@@ -337,17 +351,32 @@ __global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
     for (int i = 0; i < ITEMS; ++i)
       if (item_v<VEC>(v0, i) >= V) bits &= ~(1u << i);
   }
-  while (bits) {
-    const int i = __ffs(bits) - 1;
-    bits &= bits - 1;
-    const int pos = atomicAdd(&sm_n, 1);
-    if (pos < CAND_CAP) sm_cand[pos] = row_key(sel_item(val, i), item_v<VEC>(v0, i));
+  if (bits) {
+    float* stg = sm_stage + threadIdx.x * ITEMS;
+    if (!sval) {
+#pragma unroll
+      for (int q = 0; q < ITEMS / 4; ++q)
+        reinterpret_cast<float4*>(stg)[q] = make_float4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]);
+    }
+    do {
+      const int i = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int v = item_v<VEC>(v0, i);
+      const int pos = atomicAdd(&sm_n, 1);
+      if (pos < CAND_CAP) sm_cand[pos] = row_key(sval ? sval[v - v0] : stg[i], v);
+    } while (bits);
   }
   __syncthreads();
   const size_t o = (size_t)row * a.chunks + c;
   uint64_t* ctop = a.chunk_top + o * a.b;
   const int n_cand = sm_n;
-  if (n_cand <= CAND_CAP) {
+  if (n_cand <= 32) {  // common case: one warp sorts the candidates
+    if (w == 0) {
+      uint64_t key = lane < n_cand ? sm_cand[lane] : 0ull;
+      key = warp_sort_desc_u64(key);
+      if (lane < k) ctop[lane] = key;
+    }
+  } else if (n_cand <= CAND_CAP) {
     block_rank_topk(sm_cand, n_cand, k, ctop);
   } else {  // ties overflowed the buffer: warp arg-max rounds over the registers
     // k rounds of warp arg-max; keys are rebuilt from val[] (a taken-bit per item)
@@ -385,19 +414,16 @@ __global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
   }
   if (threadIdx.x == 0) {
     float tot = 0.f;
-    for (int i = 0; i < BS / 32; ++i) tot += sm_red[i];
+    for (int i = 0; i < BS / 32; ++i) tot += sm_sum[i];
     a.chunk_max[o] = m;
     a.chunk_sum[o] = tot;
   }
   // ---- ticket: the last chunk CTA of this row continues --------------------------------
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();  // the CTA's writes (ordered by the barrier) before the ticket
-    sm_last = atomicAdd(&a.cnt_row[row], 1u) == (unsigned)(a.chunks - 1);
-  }
+  if (threadIdx.x == 0)  // release: the CTA's writes (ordered by the barrier) before the ticket
+    sm_last = ticket_acq_rel(&a.cnt_row[row]) == (unsigned)(a.chunks - 1);
   __syncthreads();
   if (!sm_last) return;
-  __threadfence();
   if (threadIdx.x == 0) a.cnt_row[row] = 0u;
 
   // ---- row stage: lse and the row's top-b ------------------------------------------------
@@ -427,13 +453,9 @@ __global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
   if (threadIdx.x < k) rtop[threadIdx.x] = sm_mrg[0][threadIdx.x];
   // ---- ticket: the last row CTA of this request continues --------------------------------
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    sm_last = atomicAdd(&a.cnt_req[r], 1u) == (unsigned)(a.b_live - 1);
-  }
+  if (threadIdx.x == 0) sm_last = ticket_acq_rel(&a.cnt_req[r]) == (unsigned)(a.b_live - 1);
   __syncthreads();
   if (!sm_last) return;
-  __threadfence();
   if (threadIdx.x == 0) a.cnt_req[r] = 0u;
 
   // ---- request stage: global top-b over b_live x k survivors ------------------------------
@@ -479,6 +501,33 @@ __global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
   __syncthreads();
   append_sel(r, a.b, b_live, sp, st, ss, a.token, a.parent, a.depth, a.mask, a.leaf, a.score,
              a.nn, a.nkv, a.tlen, a.cap, a.status);
+}
+
+// Register-path kernel: grid (chunks, rows), one item per CTA (any V; the TMA kernel
+// below needs V % 4 == 0 and 16-byte aligned rows).
+template <bool VEC>
+__global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
+  const int c = blockIdx.x, row = blockIdx.y;
+  const int V = a.V, v0 = c * CHUNK;
+  const float* x = a.logits + (size_t)row * V;
+  float val[ITEMS];
+  if (VEC) {
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll
+    for (int q = 0; q < ITEMS / 4; ++q) {
+      const int e = item_v<true>(v0, 4 * q);
+      float4 f = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      if (e < V) f = __ldcs(x4 + (e >> 2));  // V % 4 == 0: all four valid
+      val[4 * q + 0] = f.x; val[4 * q + 1] = f.y; val[4 * q + 2] = f.z; val[4 * q + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int e = item_v<false>(v0, i);
+      val[i] = e < V ? __ldcs(x + e) : -INFINITY;
+    }
+  }
+  beam_item<VEC>(a, row, c, val, nullptr);
 }
 
 int launch_beam_step(trie_handle* h, const float* logits, int32_t* out_par, int32_t* out_tok,
