@@ -169,9 +169,14 @@ __global__ void __launch_bounds__(512) k_attn_v1(const AttnParams p) {
   }
 }
 
-// merge split partials: one warp per (r, h, query)
-template <typename T>
-__global__ void k_attn_combine(const AttnParams p) {
+// merge split partials: one warp per (r, h, query); lane c owns columns lane + 32 c
+// (c < DC = ceil(D / 32)).  The splits' (m, l) pairs are loaded lane-parallel (<= 64
+// splits), then the partial rows in batches of SB splits whose loads are all issued
+// before any is consumed (SB * DC <= 64 registers), so a launch costs ~ceil(splits / SB)
+// L2 round trips.
+template <typename T, int DC>
+__global__ void __launch_bounds__(128) k_attn_combine(const AttnParams p) {
+  constexpr int SB = DC <= 2 ? 32 : DC <= 4 ? 16 : 8;
   const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -198,19 +203,17 @@ __global__ void k_attn_combine(const AttnParams p) {
   T* op = (T*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
   const float inv = L > 0.f ? 1.f / L : 0.f;
   if (L == 0.f && lane == 0) latch(p.status, TRIE_ST_EMPTY_ROW);
-  float acc[8];
+  float acc[DC];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) acc[c] = 0.f;
-  // batches of 4 splits: all loads of a batch are issued before any is consumed
-  constexpr int SB = 4;
+  for (int c = 0; c < DC; ++c) acc[c] = 0.f;
   for (int s0 = 0; s0 < p.splits; s0 += SB) {
-    float v[SB][8];
+    float v[SB][DC];
 #pragma unroll
     for (int u = 0; u < SB; ++u) {
-      const int s = s0 + u;
-      const float* pp = base + ((size_t)min(s, p.splits - 1) * Qg + m) * (D + 2);
+      const int s = min(s0 + u, p.splits - 1);
+      const float* pp = base + ((size_t)s * Qg + m) * (D + 2);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) v[u][c] = (lane + 32 * c < D) ? __ldg(pp + lane + 32 * c) : 0.f;
+      for (int c = 0; c < DC; ++c) v[u][c] = (lane + 32 * c < D) ? __ldcg(pp + lane + 32 * c) : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < SB; ++u) {
@@ -218,16 +221,34 @@ __global__ void k_attn_combine(const AttnParams p) {
       const float w = __shfl_sync(0xffffffffu, ws[(s >> 5) & 1], s & 31);
       if (s < p.splits) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[c] += w * v[u][c];
+        for (int c = 0; c < DC; ++c) acc[c] += w * v[u][c];
       }
     }
   }
 #pragma unroll
-  for (int c = 0; c < 8; ++c)
+  for (int c = 0; c < DC; ++c)
     if (lane + 32 * c < D) op[lane + 32 * c] = from_f<T>(acc[c] * inv);
   if (p.lse && lane == 0)
     p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
         L > 0.f ? (M + log2f(L)) * 0.69314718055994531f : -INFINITY;
+}
+
+template <typename T>
+static int launch_combine_t(const AttnParams& p, cudaStream_t s) {
+  const int Qg = p.b_live * (p.Hq / p.Hkv);
+  const int warps = p.R * p.Hkv * Qg;
+  const dim3 grid((warps * 32 + 127) / 128);
+  switch ((p.D + 31) / 32) {
+    case 1: k_attn_combine<T, 1><<<grid, 128, 0, s>>>(p); break;
+    case 2: k_attn_combine<T, 2><<<grid, 128, 0, s>>>(p); break;
+    case 3: k_attn_combine<T, 3><<<grid, 128, 0, s>>>(p); break;
+    case 4: k_attn_combine<T, 4><<<grid, 128, 0, s>>>(p); break;
+    case 5: k_attn_combine<T, 5><<<grid, 128, 0, s>>>(p); break;
+    case 6: k_attn_combine<T, 6><<<grid, 128, 0, s>>>(p); break;
+    case 7: k_attn_combine<T, 7><<<grid, 128, 0, s>>>(p); break;
+    default: k_attn_combine<T, 8><<<grid, 128, 0, s>>>(p); break;
+  }
+  return trie_check_launch("k_attn_combine");
 }
 
 template <typename T>
@@ -263,19 +284,12 @@ static int launch_v1_t(const AttnParams& p, cudaStream_t s) {
 #undef V1_CASE
   int rc = trie_check_launch("k_attn_v1");
   if (rc) return rc;
-  if (p.splits > 1) {
-    const int warps = p.R * p.Hkv * Qg;
-    k_attn_combine<T><<<(warps * 32 + 255) / 256, 256, 0, s>>>(p);
-    rc = trie_check_launch("k_attn_combine");
-  }
+  if (p.splits > 1) rc = launch_combine_t<T>(p, s);
   return rc;
 }
 
 int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s) {
-  const int Qg = p.b_live * (p.Hq / p.Hkv);
-  const int warps = p.R * p.Hkv * Qg;
-  k_attn_combine<__nv_bfloat16><<<(warps * 32 + 255) / 256, 256, 0, s>>>(p);
-  return trie_check_launch("k_attn_combine");
+  return launch_combine_t<__nv_bfloat16>(p, s);
 }
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s) {

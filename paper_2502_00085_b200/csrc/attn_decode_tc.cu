@@ -74,8 +74,8 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     }
     mbar_init(app_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    item_setup(p, r, split, info);
   }
+  if (threadIdx.x < 32) item_setup(p, r, split, info);
   __syncthreads();
   const ItemInfo it = *info;
   if (warp == 0) {
@@ -416,8 +416,8 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       mbar_init(&empty[s], C::NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    item_setup(p, r, split, info);
   }
+  if (threadIdx.x < 32) item_setup(p, r, split, info);
   __syncthreads();
   const ItemInfo it = *info;
   if (warp == 0) {

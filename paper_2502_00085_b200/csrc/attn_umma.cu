@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
       mbar_init(&pv_done[e], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    item_setup(p, r, split, info);
   }
+  if (threadIdx.x < 32) item_setup(p, r, split, info);
   if (warp == 1) {  // TMEM allocation (whole warp), address published through smem
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),

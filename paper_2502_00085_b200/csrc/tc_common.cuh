@@ -106,39 +106,62 @@ struct ItemInfo {
   int tile0, ntiles, lo, N, t, fast_from;
 };
 
-// Thread 0: tile range of this (r, split) and the first tile index from which the mask
-// is needed (tiles below it are prompt-only and inside every beam's window).
+// Whole warp 0 (lane 0 writes *info): tile range of this (r, split) and the first tile
+// index from which the mask is needed (tiles below it are prompt-only and inside every
+// beam's window).  Few dependent global loads: the leaves' depths in parallel (one per
+// lane), then the window's first slot.  That slot is the first n with depth[n] >= lo_dep
+// (depth is non-decreasing in slot order, invariant 1); on the prompt chain depth[n] = n
+// (Alg. 2 l.1), so lo_dep itself is probed first and a 32-ary search only runs if the
+// probe fails (lo_dep beyond the prompt or a non-standard trie).
 __device__ __forceinline__ void item_setup(const AttnParams& p, int r, int split, ItemInfo* info) {
+  const int lane = threadIdx.x & 31;
   const size_t mbase = (size_t)r * p.cap;
   const int N = p.nn[r], t = p.tlen[r];
   int lo = 0, lo_dep_max = INT_MIN;
   if (p.window > 0) {
-    int lo_dep = INT_MAX;
-    for (int j = 0; j < p.b_live; ++j) {
-      const int d = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + j]] - p.window + 1;
-      lo_dep = min(lo_dep, d);
-      lo_dep_max = max(lo_dep_max, d);
+    int dl = INT_MAX, dh = INT_MIN;
+    if (lane < p.b_live) {
+      dl = dh = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + lane]] - p.window + 1;
     }
-    int a = 0, b = N;  // first slot with depth >= lo_dep (depth non-decreasing)
-    while (a < b) {
-      const int mid = (a + b) >> 1;
-      if (p.depth[mbase + mid] < lo_dep) a = mid + 1; else b = mid;
+    const int lo_dep = __reduce_min_sync(0xffffffffu, dl);
+    lo_dep_max = __reduce_max_sync(0xffffffffu, dh);
+    if (lo_dep > 0) {
+      bool found = false;
+      if (lo_dep < N) {  // probe: depth[lo_dep - 1] < lo_dep <= depth[lo_dep]
+        const int pr = lane < 2 ? p.depth[mbase + lo_dep - 1 + lane] : 0;
+        const int d0 = __shfl_sync(0xffffffffu, pr, 0), d1 = __shfl_sync(0xffffffffu, pr, 1);
+        found = d0 < lo_dep && d1 >= lo_dep;
+        lo = lo_dep;
+      }
+      if (!found) {  // answer in [a, b]: depth < lo_dep below a; b == N or depth[b] >= lo_dep
+        int a = 0, b = N;
+        while (a < b) {
+          const int step = (b - a + 31) / 32;
+          const int pos = a + lane * step;
+          const bool ge = pos >= b || p.depth[mbase + pos] >= lo_dep;
+          const int first = __ffs(__ballot_sync(0xffffffffu, ge)) - 1;
+          const int nb = min(b, a + first * step);
+          a = first == 0 ? a : a + (first - 1) * step + 1;
+          b = nb;
+        }
+        lo = a;
+      }
     }
-    lo = a;
   }
   const int first = lo / TC_TR;
   const int total = (N + TC_TR - 1) / TC_TR - first;
   const int per = (total + p.splits - 1) / p.splits;
   const int tb = min(total, split * per), te = min(total, (split + 1) * per);
-  info->tile0 = first + tb;
-  info->ntiles = te - tb;
-  info->lo = lo;
-  info->N = N;
-  info->t = t;
-  // unmasked tiles: every row n satisfies n < t (prompt: depth = n), n < N and
-  // depth = n >= every beam's lower depth  <=>  tile in [ceil(lo_dep_max / TR), t / TR)
-  const int fmin = p.window > 0 ? (max(lo_dep_max, 0) + TC_TR - 1) / TC_TR : 0;
-  info->fast_from = fmin;  // fast tiles: fmin <= tile < min(t, N) / TR
+  if (lane == 0) {
+    info->tile0 = first + tb;
+    info->ntiles = te - tb;
+    info->lo = lo;
+    info->N = N;
+    info->t = t;
+    // unmasked tiles: every row n satisfies n < t (prompt: depth = n), n < N and
+    // depth = n >= every beam's lower depth  <=>  tile in [ceil(lo_dep_max / TR), t / TR)
+    info->fast_from = p.window > 0 ? (max(lo_dep_max, 0) + TC_TR - 1) / TC_TR : 0;
+  }
 }
 
 template <int D, int STAGES>
