@@ -263,6 +263,7 @@ static AttnPlan attn_plan(const trie_cfg* c, int b_live, int rows_hint, bool rop
   const int rows = rows_hint > 0 ? rows_hint : c->capacity;
   trie::AttnParams sp = shape_params(c, b_live);
   sp.rope = rope ? 1 : 0;
+  sp.rows_hint = rows;
   pl.persist = trie::attn_persist_enabled() && trie::attn_tc_shape_ok(sp);
   if (pl.persist) {
     pl.splits = trie::attn_persist_splits(sp, rows, sm_count());
@@ -306,6 +307,7 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
     beam_mask = derived;
   }
   trie::AttnParams p = shape_params(cfg, b_live);
+  p.rows_hint = rows_hint > 0 ? rows_hint : cfg->capacity;
   p.q = q;
   p.k = k_pool;
   p.v = v_pool;
@@ -333,6 +335,7 @@ int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,
   if (!info_host || b_live < 1 || b_live > cfg->beam_width)
     return trie_set_error(TRIE_EINVAL, "bad argument");
   trie::AttnParams p = shape_params(cfg, b_live);
+  p.rows_hint = rows_hint > 0 ? rows_hint : cfg->capacity;
   const AttnPlan pl = attn_plan(cfg, b_live, rows_hint);
   const int Qg = b_live * (cfg->n_q_heads / cfg->n_kv_heads);
   int path = 0;
@@ -358,6 +361,7 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   const trie_cfg* cfg = &h->cfg;
   const int b_live = h->b_live;
   trie::AttnParams p = shape_params(cfg, b_live);
+  p.rows_hint = rows_hint > 0 ? rows_hint : cfg->capacity;
   p.q = q;
   p.k = k_pool;
   p.v = v_pool;

@@ -19,6 +19,7 @@ struct AttnParams {
   void* aux;              // persistent path: zero-initialised queue / item counters
   uint32_t* status;
   int R, b_live, Hq, Hkv, D, cap, window, splits;
+  int rows_hint;          // expected rows per request (planning only; 0 = capacity)
   float scale_log2;       // log2(e) / sqrt(D)
   int bf16;
   // fused RoPE + KV append (trie_attn_decode_rope): q is read un-rotated, the leaves'

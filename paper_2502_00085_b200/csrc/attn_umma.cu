@@ -578,18 +578,26 @@ static const UKernel* select_u(int D) {
 }
 
 // tcgen05 path for Qg in [umma_min_qg, 128]; TRIE_UMMA_MIN_QG overrides (0 disables)
+// Which query groups take the tcgen05 kernel.  Default (measured r20, D = 128): every
+// Qg >= 33 (mma.sync is tensor-pipe bound there), and Qg >= 9 when a request holds
+// >= 1024 rows (sweep t = 8192: Qg = 16 6.22 vs 5.97 TB/s narrow, Qg = 32 6.10 vs 5.95
+// wide; Mistral shard Qg = 16: 16.5 vs 19.2 us) -- its fixed per-CTA cost (TMEM
+// allocation, barrier setup) loses on short tries (Llama t = 150: 26.8 vs 14.2 us).
+// TRIE_UMMA_MIN_QG = n overrides with the plain rule Qg >= n (0 disables).
 int attn_umma_min_qg() {
-  static int v = -1;
-  if (v < 0) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("TRIE_UMMA_MIN_QG");
-    v = e ? atoi(e) : 33;
+    v = e ? atoi(e) : -1;
   }
   return v;
 }
 bool attn_umma_eligible(const AttnParams& p) {
   const int Qg = p.b_live * (p.Hq / p.Hkv);
+  if (Qg > 128 || !attn_tc_shape_ok(p)) return false;
   const int mn = attn_umma_min_qg();
-  return mn > 0 && Qg >= mn && Qg <= 128 && attn_tc_shape_ok(p);
+  if (mn >= 0) return mn > 0 && Qg >= mn;
+  return Qg >= 33 || (Qg >= 9 && p.D == 128 && p.rows_hint >= 1024);
 }
 int attn_umma_occ(const AttnParams& p) {
   const UKernel* k = select_u(p.D);
