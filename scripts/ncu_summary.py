@@ -1,6 +1,8 @@
 """Summarise ncu captures (run here, on the CPU box) into profiles/.
 
     python scripts/ncu_summary.py <tag> <workload> <launches.csv> <attn.ncu-rep> [aux.ncu-rep]
+        [--requests R --beam b]   (recorded with the dram bytes; bench.py uses them only
+                                   for the same workload, requests and beam width)
 
 Writes profiles/<tag>_<workload>_launches.md (per-kernel share of the step from the
 gpu__time_duration launch list), profiles/<tag>_<workload>_ncu.md (key --set full metrics
@@ -66,8 +68,15 @@ def to_bytes(v, u):
 
 
 def main():
-    tag, wl, lcsv, attn = sys.argv[1:5]
-    aux = sys.argv[5] if len(sys.argv) > 5 else None
+    argv = list(sys.argv[1:])
+    opts = {}
+    for key in ("--requests", "--beam"):
+        if key in argv:
+            i = argv.index(key)
+            opts[key[2:]] = int(argv[i + 1])
+            del argv[i:i + 2]
+    tag, wl, lcsv, attn = argv[:4]
+    aux = argv[4] if len(argv) > 4 else None
     os.makedirs(PROF, exist_ok=True)
     table, _ = launches(lcsv)
     with open(os.path.join(PROF, f"{tag}_{wl}_launches.md"), "w") as f:
@@ -89,7 +98,7 @@ def main():
     js = os.path.join(PROF, "ncu_attn_summary.json")
     d = json.load(open(js)) if os.path.exists(js) else {}
     if dram:
-        d[wl] = {"tag": tag, "dram_bytes_per_launch": sum(dram) / len(dram), "captures": len(dram)}
+        d[wl] = {"tag": tag, "dram_bytes_per_launch": sum(dram) / len(dram), "captures": len(dram), **opts}
     json.dump(d, open(js, "w"), indent=1)
     print("wrote", tag, wl, "attn dram/launch", d.get(wl))
 

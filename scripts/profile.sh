@@ -13,6 +13,6 @@ $NCU --metrics gpu__time_duration.sum --clock-control none -k regex:"^k_|trie" -
 $NCU --set full --clock-control none --import-source on -k regex:k_attn -s 200 -c 2 \
      -o gpurun_out/attn_${TAG} -f python bench.py $ARGS > gpurun_out/attn_${TAG}.log 2>&1
 # 3) beam-step and prune kernels, one capture each
-$NCU --set full --clock-control none -k regex:"k_row_chunk|k_select_append|k_prune_scan|k_kv_compact|k_rope" -s 20 -c 5 \
+$NCU --set full --clock-control none -k regex:"k_beam_step|k_prune_scan|k_kv_compact|k_rope" -s 20 -c 5 \
      -o gpurun_out/aux_${TAG} -f python bench.py $ARGS > gpurun_out/aux_${TAG}.log 2>&1
 ls -la gpurun_out/
