@@ -40,9 +40,12 @@ WORKLOADS = {
     # configs[2]: request-parallel over 1/2/4/8 GPUs (R per GPU)
     "llama": dict(name="llama3.1-8b-gqa-humaneval-t150-b8-s256", L=32, Hq=32, Hkv=8, D=128,
                   V=128256, t=150, b=8, s=256, R=32, W=0, theta=500000.0),
-    # configs[3], one rank's shard: 1 KV head + 4 query heads of 8, W = 4096 (reading A15)
-    "mistral-shard": dict(name="mistral-small-24b-swa-t4096-b4-s128-kvshard1of8", L=40, Hq=4, Hkv=1,
-                          D=128, V=131072, t=4096, b=4, s=128, R=16, W=4096, theta=1e8),
+    # configs[3]: Mistral-Small-24B-shaped SWA, W = 4096 (reading A15); the 8 KV heads are
+    # sharded over the N ranks (8/N KV heads + their 32/N query heads each, the SAME R
+    # requests on every rank) with a per-layer all-gather of the attention outputs
+    # (paper_2502_00085_b200/dist.py); strong scaling: the job is fixed, N = 1 holds all heads
+    "mistral-shard": dict(name="mistral-small-24b-swa-t4096-b4-s128-kvshard", L=40, Hq=32, Hkv=8,
+                          D=128, V=131072, t=4096, b=4, s=128, R=16, W=4096, theta=1e8, kv_shard=True),
     # configs[4] kernel-level sweep point (b set by --beam)
     "sweep": dict(name="llama3.1-8b-gqa-t8192-sweep", L=4, Hq=32, Hkv=8, D=128, V=128256, t=8192,
                   b=16, s=128, R=16, W=0, theta=500000.0),  # SURVEY cfg5: R in {1, 4, 16}
@@ -104,22 +107,32 @@ class Clocks:
 class HotPath:
     """Buffers, trie state and captured step graphs for one rank."""
 
-    def __init__(self, wl, rank, dev):
+    def __init__(self, wl, rank, dev, world=1):
         import torch
 
         from paper_2502_00085_b200.trie import TrieState
+        from paper_2502_00085_b200 import dist as tdist
         import synth
         self.torch = torch
         self.wl = wl
         L, Hq, Hkv, D, V, t, b, s, R, W = (wl[k] for k in ("L", "Hq", "Hkv", "D", "V", "t", "b", "s", "R", "W"))
+        self.kv_shard = bool(wl.get("kv_shard"))
+        self.world = world
+        if self.kv_shard:  # this rank's KV heads and their query heads
+            _, Hkv, _, Hq = tdist.kv_head_shard(Hq, Hkv, world, rank)
         self.L, self.Hq, self.Hkv, self.D, self.V, self.t, self.b, self.s, self.R, self.W = \
             L, Hq, Hkv, D, V, t, b, s, R, W
         self.cap = (t + b * s + b + 63) // 64 * 64  # whole 64-slot tiles (TMA path: cap % 4 == 0)
         self.dev = dev
         gen = torch.Generator(device=dev)
         gen.manual_seed(1234 + rank)
-        # request-parallel partition: this rank owns its own R requests (weak scaling)
-        prompts, lens = synth.prompts(10_000 + rank, R, t, V)
+        # logits drive the beam step: identical on every rank of a KV-head shard (same
+        # requests, same selections, same trie metadata)
+        lgen = torch.Generator(device=dev)
+        lgen.manual_seed(4321 + (0 if self.kv_shard else rank))
+        # request-parallel partition: this rank owns its own R requests (weak scaling);
+        # KV-head shard: every rank holds the same R requests
+        prompts, lens = synth.prompts(10_000 + (0 if self.kv_shard else rank), R, t, V)
         self.st = TrieState(R, b, t, self.cap, L, Hq, Hkv, D, V, prompts, lens, window=W,
                             dtype=torch.bfloat16, device=dev)
         self.kp, self.vp = self.st.new_pools()
@@ -133,7 +146,7 @@ class HotPath:
             per_layer = R * bl * (Hq + 2 * Hkv) * D
             for slot in range(self.NB):
                 qkv = torch.randn(L * per_layer, device=dev, generator=gen).to(torch.bfloat16)
-                lg = torch.randn(R * bl * V, device=dev, generator=gen) * 3.0
+                lg = torch.randn(R * bl * V, device=dev, generator=lgen) * 3.0
                 views = []
                 for l in range(L):
                     base = l * per_layer
@@ -143,6 +156,11 @@ class HotPath:
                     views.append((q, k, v))
                 self.inp[(var, slot)] = dict(qkv=qkv, logits=lg.view(R, bl, V), views=views,
                                              out=torch.empty(R, bl, Hq, D, dtype=torch.bfloat16, device=dev))
+        # all-gather target of the attention outputs (KV-head shard, N > 1)
+        self.gathered = (torch.empty(world, R, b, Hq, D, dtype=torch.bfloat16, device=dev)
+                         if self.kv_shard and world > 1 else None)
+        self.gathered1 = (torch.empty(world, R, 1, Hq, D, dtype=torch.bfloat16, device=dev)
+                          if self.gathered is not None else None)
         self.sel_p = torch.empty(R, b, dtype=torch.int32, device=dev)
         self.sel_t = torch.empty_like(self.sel_p)
         self.sel_s = torch.empty(R, b, dtype=torch.float32, device=dev)
@@ -179,10 +197,17 @@ class HotPath:
             st.attn_decode(q, self.kp[l], self.vp[l], d["out"], rows_hint=self.rows_hint)
             if events is not None:
                 events[l][1].record()
+            if self.gathered is not None:  # KV-head shard: every rank needs every head
+                self._gather(d["out"])
         if events is not None and fused:
             events[0][1].record()
         st.beam_step(d["logits"], self.sel_p, self.sel_t, self.sel_s)
         st.prune_compact(self.kp, self.vp)
+
+    def _gather(self, out):
+        from paper_2502_00085_b200.dist import gather_heads
+        # the first step of a job has one live beam: its own buffer
+        gather_heads(out, self.gathered if out.shape[1] == self.b else self.gathered1)
 
     def capture(self):
         """One graph per (variant, slot) + an event-instrumented twin for kernel timing."""
@@ -289,7 +314,9 @@ def run_gpu(args):
         wl["b"] = args.beam
     if args.requests:
         wl["R"] = args.requests
-    hp = HotPath(wl, rank, dev)
+    if wl.get("kv_shard") and world > 1 and backend != "nccl":
+        raise SystemExit("the KV-head shard's per-layer all-gather is captured in CUDA graphs: NCCL only")
+    hp = HotPath(wl, rank, dev, world)
     R, L, s, b, t = hp.R, hp.L, hp.s, hp.b, hp.t
 
     # eager warm-up (allocates scratch, sets kernel attributes), then capture
@@ -384,15 +411,20 @@ def run_gpu(args):
     ach = c_bytes / (c_us * 1e-6) / 1e9
     peak, peak_src = _peaks()
 
-    value = R * args.steps * world / (ms * 1e-3)
+    # request-DP: every rank its own R requests; KV-head shard: the same R on every rank
+    units = R if hp.kv_shard else R * world
+    value = units * args.steps / (ms * 1e-3)
     kv_fp = R * (t + s // 2) * hp.Hkv * hp.D * 4 * L
     res = dict(metric="beam-decode steps/s (request-steps/s, hot path) + trie-attn HBM GB/s",
                value=round(value, 2), unit="request-steps/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(ms / args.steps, 4), higher_is_better=True,
-               scaling="weak", vs_baseline=None, dtype="bf16", data="synthetic",
+               scaling="strong" if hp.kv_shard else "weak", vs_baseline=None, dtype="bf16", data="synthetic",
                config=dict(workload=wl["name"], requests_per_gpu=R, beam=b, prompt_len=t,
-                           new_tokens=s, layers=L, q_heads=hp.Hq, kv_heads=hp.Hkv, head_dim=hp.D,
-                           vocab=hp.V, window=hp.W, gc_interval=1, parallelism=f"request-dp{world}",
+                           new_tokens=s, layers=L, q_heads_per_gpu=hp.Hq, kv_heads_per_gpu=hp.Hkv,
+                           head_dim=hp.D,
+                           vocab=hp.V, window=hp.W, gc_interval=1,
+                           parallelism=(f"kv-head-shard{world} (per-layer all-gather of attention outputs)"
+                                        if hp.kv_shard else f"request-dp{world}"),
                            execution="cuda-graph replay per step",
                            attention={k: v for k, v in hp.plan["steady"].items()},
                            l2=(f"no flush: each layer's pool is re-read once per step and the per-step "
@@ -491,7 +523,8 @@ def run_e2e(hp, args, world):
         tt = torch.tensor([ms], device=hp.dev if os.environ.get("BENCH_DIST_BACKEND", "nccl") == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    return {"value": round(hp.R * args.steps * world / (ms * 1e-3), 2), "unit": "request-steps/s",
+    units = hp.R if hp.kv_shard else hp.R * world
+    return {"value": round(units * args.steps / (ms * 1e-3), 2), "unit": "request-steps/s",
             "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
             "ms_per_step": round(ms / args.steps, 4),
             "path": "C ABI via the binding; pinned host -> device copies on a side stream, "

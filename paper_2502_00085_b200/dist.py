@@ -1,7 +1,18 @@
-"""Request data parallelism: one process per GPU, each owning a
-contiguous block of independent requests ("distinct sessions may run in parallel").
-There is no per-step collective: ranks decode their own requests; the only collectives are
-the end-of-job gather of the hypotheses and the max-over-ranks timing reduction.
+"""Multi-GPU plumbing; one process per GPU.
+
+Request data parallelism: each rank owns a contiguous block of independent requests
+("distinct sessions may run in parallel").  No per-step collective: ranks decode
+their own requests; the only collectives are the end-of-job gather of the hypotheses and
+the max-over-ranks timing reduction.
+
+KV-head sharding (BASELINE.json configs[3], the 24B shape): every rank holds the SAME
+requests and trie metadata but only its slice of the KV heads (Hkv / world KV heads and
+their Hq / world query heads, GQA groups kept whole).  Per layer each rank runs
+trie_attn_decode on its slice and the attention outputs are all-gathered so that the
+replicated O-projection / MLP / LM head (model context) see every head; identical logits
+then give identical beam-step choices and identical trie metadata on every rank, and each
+rank prunes / compacts only its own KV slice.
+
 Works with any torch.distributed backend (NCCL on the GPU box, gloo in the CPU tests).
 """
 from __future__ import annotations
@@ -45,3 +56,38 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def kv_head_shard(n_q_heads: int, n_kv_heads: int, world: int, rank: int):
+    """This rank's KV heads [kv0, kv0 + n_kv) and query heads [q0, q0 + n_q): contiguous
+    blocks of whole GQA groups (query head h uses KV head h // (Hq / Hkv), S:104)."""
+    if n_q_heads % n_kv_heads:
+        raise ValueError("n_q_heads must be a multiple of n_kv_heads")
+    if world < 1 or not (0 <= rank < world) or n_kv_heads % world:
+        raise ValueError(f"{n_kv_heads} KV heads cannot be split over {world} ranks")
+    n_kv = n_kv_heads // world
+    g = n_q_heads // n_kv_heads
+    return rank * n_kv, n_kv, rank * n_kv * g, n_kv * g
+
+
+def gather_heads(out_local: torch.Tensor, gathered: torch.Tensor | None = None) -> torch.Tensor:
+    """All-gather of the per-rank attention outputs [R][b][Hq/world][D] into the rank-major
+    buffer [world][R][b][Hq/world][D] (one collective per layer; CUDA-graph capturable
+    under NCCL).  `gathered` may be preallocated (the bench captures it in its graphs)."""
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    if gathered is None:
+        gathered = out_local.new_empty((world,) + tuple(out_local.shape))
+    if world == 1:
+        gathered[0].copy_(out_local)
+        return gathered
+    if gathered.is_cuda:
+        dist.all_gather_into_tensor(gathered, out_local.contiguous())
+    else:  # gloo (CPU tests): list form
+        dist.all_gather(list(gathered.unbind(0)), out_local.contiguous())
+    return gathered
+
+
+def heads_view(gathered: torch.Tensor) -> torch.Tensor:
+    """[world][R][b][Hq/world][D] -> [R][b][Hq][D] in global head order (a copy)."""
+    w, R, b, hl, D = gathered.shape
+    return gathered.permute(1, 2, 0, 3, 4).reshape(R, b, w * hl, D)
