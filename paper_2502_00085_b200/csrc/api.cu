@@ -1,5 +1,6 @@
 // C ABI glue of libtriedecode: argument validation, workspace carving, dispatch.
 // Every step of the hot path runs in the kernels of this library; there is no CPU path.
+#include <stdlib.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -49,6 +50,15 @@ static int validate(const trie_cfg* c) {
   if (c->kv_dtype != TRIE_F32 && c->kv_dtype != TRIE_BF16)
     return trie_set_error(TRIE_EINVAL, "kv_dtype");
   return TRIE_OK;
+}
+
+bool trie::pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TRIE_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }

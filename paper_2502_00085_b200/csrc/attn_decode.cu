@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(512) k_attn_v1(const AttnParams p) {
 // L2 round trips.
 template <typename T, int DC>
 __global__ void __launch_bounds__(128) k_attn_combine(const AttnParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int SB = DC <= 2 ? 32 : DC <= 4 ? 16 : 8;
   const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -239,14 +241,14 @@ static int launch_combine_t(const AttnParams& p, cudaStream_t s) {
   const int warps = p.R * p.Hkv * Qg;
   const dim3 grid((warps * 32 + 127) / 128);
   switch ((p.D + 31) / 32) {
-    case 1: k_attn_combine<T, 1><<<grid, 128, 0, s>>>(p); break;
-    case 2: k_attn_combine<T, 2><<<grid, 128, 0, s>>>(p); break;
-    case 3: k_attn_combine<T, 3><<<grid, 128, 0, s>>>(p); break;
-    case 4: k_attn_combine<T, 4><<<grid, 128, 0, s>>>(p); break;
-    case 5: k_attn_combine<T, 5><<<grid, 128, 0, s>>>(p); break;
-    case 6: k_attn_combine<T, 6><<<grid, 128, 0, s>>>(p); break;
-    case 7: k_attn_combine<T, 7><<<grid, 128, 0, s>>>(p); break;
-    default: k_attn_combine<T, 8><<<grid, 128, 0, s>>>(p); break;
+    case 1: launch_k(k_attn_combine<T, 1>, grid, dim3(128), 0, s, p); break;
+    case 2: launch_k(k_attn_combine<T, 2>, grid, dim3(128), 0, s, p); break;
+    case 3: launch_k(k_attn_combine<T, 3>, grid, dim3(128), 0, s, p); break;
+    case 4: launch_k(k_attn_combine<T, 4>, grid, dim3(128), 0, s, p); break;
+    case 5: launch_k(k_attn_combine<T, 5>, grid, dim3(128), 0, s, p); break;
+    case 6: launch_k(k_attn_combine<T, 6>, grid, dim3(128), 0, s, p); break;
+    case 7: launch_k(k_attn_combine<T, 7>, grid, dim3(128), 0, s, p); break;
+    default: launch_k(k_attn_combine<T, 8>, grid, dim3(128), 0, s, p); break;
   }
   return trie_check_launch("k_attn_combine");
 }

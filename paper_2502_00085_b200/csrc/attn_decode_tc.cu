@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
   ItemInfo* info = (ItemInfo*)(app_done + 1);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -75,6 +76,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     mbar_init(app_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // the shared-memory setup above ran before the predecessor finished
   if (threadIdx.x < 32) item_setup(p, r, split, info);
   __syncthreads();
   const ItemInfo it = *info;
@@ -409,6 +411,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
   ItemInfo* info = (ItemInfo*)(empty + C::STAGES);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -417,6 +420,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // the shared-memory setup above ran before the predecessor finished
   if (threadIdx.x < 32) item_setup(p, r, split, info);
   __syncthreads();
   const ItemInfo it = *info;
@@ -835,7 +839,7 @@ int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
   if (rc) return rc;
   AttnParams pp = p;
   void* args[3] = {(void*)&km, (void*)&vm, (void*)&pp};
-  cudaLaunchKernel(k->fn, dim3(p.Hkv, p.R, p.splits), dim3(k->threads), args, (size_t)k->smem, s);
+  launch_k_ptr(k->fn, dim3(p.Hkv, p.R, p.splits), dim3(k->threads), (size_t)k->smem, s, args);
   rc = trie_check_launch("k_attn_tc");
   if (rc) return rc;
   if (p.splits > 1) rc = launch_attn_combine_bf16(p, s);

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
   ItemInfo* info = (ItemInfo*)(tmem_slot + 4);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
   const int n_live = min(4, (Qg + 31) / 32);  // sub-partitions holding real query rows
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // the shared-memory setup above ran before the predecessor finished
   if (threadIdx.x < 32) item_setup(p, r, split, info);
   if (warp == 1) {  // TMEM allocation (whole warp), address published through smem
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -614,7 +616,7 @@ int launch_attn_umma(const AttnParams& p, cudaStream_t s) {
   if (rc) return rc;
   AttnParams pp = p;
   void* args[3] = {(void*)&km, (void*)&vm, (void*)&pp};
-  cudaLaunchKernel(k->fn, dim3(p.Hkv, p.R, p.splits), dim3(k->threads), args, (size_t)k->smem, s);
+  launch_k_ptr(k->fn, dim3(p.Hkv, p.R, p.splits), dim3(k->threads), (size_t)k->smem, s, args);
   rc = trie_check_launch("k_attn_umma");
   if (rc) return rc;
   if (p.splits > 1) rc = launch_attn_combine_bf16(p, s);

@@ -507,6 +507,8 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
 // below needs V % 4 == 0 and 16-byte aligned rows).
 template <bool VEC>
 __global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int c = blockIdx.x, row = blockIdx.y;
   const int V = a.V, v0 = c * CHUNK;
   const float* x = a.logits + (size_t)row * V;
@@ -555,9 +557,9 @@ int launch_beam_step(trie_handle* h, const float* logits, int32_t* out_par, int3
   a.out_par = out_par; a.out_tok = out_tok; a.out_sc = out_sc;
   dim3 grid(a.chunks, c.n_requests * h->b_live);
   if (vec)
-    k_beam_step<true><<<grid, BS, 0, s>>>(a);
+    launch_k(k_beam_step<true>, grid, dim3(BS), 0, s, a);
   else
-    k_beam_step<false><<<grid, BS, 0, s>>>(a);
+    launch_k(k_beam_step<false>, grid, dim3(BS), 0, s, a);
   return trie_check_launch("k_beam_step");
 }
 

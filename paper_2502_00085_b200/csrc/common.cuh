@@ -51,6 +51,48 @@ __device__ __forceinline__ void latch(uint32_t* status, uint32_t bit) {
   if (status) atomicOr(status, bit);
 }
 
+// ---- programmatic dependent launch (PDL) ---------------------------------------------------
+// Hot-path kernels are launched with programmatic stream serialization (launch_k below):
+// a kernel may be scheduled while its predecessor drains.  pdl_trigger() lets the NEXT
+// kernel's CTAs launch once every CTA of this grid has started; pdl_wait() blocks until the
+// predecessor grid has completed and its memory is visible -- every kernel calls it before
+// its first global-memory access (setup that touches only shared memory / TMEM / tensor
+// maps may run before it).  Both are no-ops for a plain launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+bool pdl_enabled();  // TRIE_PDL=0 disables (api.cu)
+
+inline void pdl_config(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* attr, dim3 grid, dim3 block,
+                       size_t smem, cudaStream_t s) {
+  cfg->gridDim = grid;
+  cfg->blockDim = block;
+  cfg->dynamicSmemBytes = smem;
+  cfg->stream = s;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg->attrs = attr;
+  cfg->numAttrs = pdl_enabled() ? 1 : 0;
+}
+
+// kernel<<<grid, block, smem, s>>>(args...) with the PDL attribute
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  pdl_config(&cfg, attr, grid, block, smem, s);
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+// the same for a kernel held as a void pointer with a packed argument array
+inline cudaError_t launch_k_ptr(const void* kern, dim3 grid, dim3 block, size_t smem,
+                                cudaStream_t s, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  pdl_config(&cfg, attr, grid, block, smem, s);
+  return cudaLaunchKernelExC(&cfg, kern, args);
+}
+
 }  // namespace trie
 
 // ---- host-side error plumbing (api.cu) --------------------------------------------------

@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(ROPE_BS) k_rope_append(
     int b_live, int Hq, int Hkv, int D, int cap) {
   constexpr int VN = Vec16<T>::N;
   __shared__ float s_cos[128], s_sin[128];  // D <= 256
+  pdl_trigger();
+  pdl_wait();
   const int rj = blockIdx.x;                // r * b_live + j
   const int r = rj / b_live;
   const int slot = leaf[r * TRIE_MAX_BEAMS + rj % b_live];
@@ -126,6 +128,8 @@ __global__ void __launch_bounds__(ROPE_BS) k_rope_append(
 __global__ void k_rope_table(float2* __restrict__ tab, const int32_t* __restrict__ depth,
                              const int32_t* __restrict__ leaf, int b_live, int D, int cap,
                              double log2_theta) {
+  pdl_trigger();
+  pdl_wait();
   const int rj = blockIdx.x, r = rj / b_live, j = rj % b_live;
   const int pos = depth[(size_t)r * cap + leaf[r * TRIE_MAX_BEAMS + j]];
   for (int i = threadIdx.x; i < D / 2; i += blockDim.x) {
@@ -138,8 +142,9 @@ __global__ void k_rope_table(float2* __restrict__ tab, const int32_t* __restrict
 
 int launch_rope_table(trie_handle* h, float theta, cudaStream_t s) {
   const trie_cfg& c = h->cfg;
-  k_rope_table<<<c.n_requests * h->b_live, 64, 0, s>>>(h->rope_tab, h->depth, h->leaf, h->b_live,
-                                                       c.head_dim, c.capacity, log2((double)theta));
+  launch_k(k_rope_table, dim3(c.n_requests * h->b_live), dim3(64), 0, s, h->rope_tab,
+           (const int32_t*)h->depth, (const int32_t*)h->leaf, h->b_live, c.head_dim, c.capacity,
+           log2((double)theta));
   return trie_check_launch("k_rope_table");
 }
 
@@ -159,15 +164,16 @@ int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, 
   if (c.kv_dtype == TRIE_BF16) {
     if ((c.head_dim / 2) % 8)
       return trie_set_error(TRIE_EINVAL, "rope_kv_append: bf16 needs head_dim % 16 == 0");
-    k_rope_append<__nv_bfloat16><<<grid, ROPE_BS, 0, s>>>(
-        (__nv_bfloat16*)q, (__nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
-        (__nv_bfloat16*)kpool, (__nv_bfloat16*)vpool, h->leaf, h->rope_tab, h->b_live,
-        c.n_q_heads, c.n_kv_heads, c.head_dim, c.capacity);
+    launch_k(k_rope_append<__nv_bfloat16>, grid, dim3(ROPE_BS), 0, s,
+             (__nv_bfloat16*)q, (__nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
+             (__nv_bfloat16*)kpool, (__nv_bfloat16*)vpool, (const int32_t*)h->leaf,
+             (const float2*)h->rope_tab, h->b_live, c.n_q_heads, c.n_kv_heads, c.head_dim,
+             c.capacity);
   } else {
-    k_rope_append<float><<<grid, ROPE_BS, 0, s>>>((float*)q, (float*)k_new, (const float*)v_new,
-                                                  (float*)kpool, (float*)vpool, h->leaf,
-                                                  h->rope_tab, h->b_live, c.n_q_heads, c.n_kv_heads,
-                                                  c.head_dim, c.capacity);
+    launch_k(k_rope_append<float>, grid, dim3(ROPE_BS), 0, s, (float*)q, (float*)k_new,
+             (const float*)v_new, (float*)kpool, (float*)vpool, (const int32_t*)h->leaf,
+             (const float2*)h->rope_tab, h->b_live, c.n_q_heads, c.n_kv_heads, c.head_dim,
+             c.capacity);
   }
   return trie_check_launch("k_rope_append");
 }

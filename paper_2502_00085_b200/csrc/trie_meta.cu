@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(PRUNE_BS) k_prune_scan(
     int32_t* nn, const int32_t* nkv, const int32_t* tlen, int32_t* newidx, int32_t* moves,
     int32_t* n_moves, int b_live, int cap, uint32_t* status) {
   __shared__ int sm_warp[32];
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const int N = nn[r], t = tlen[r], n_kv = nkv[r];
   const size_t base = (size_t)r * cap;
@@ -156,6 +158,8 @@ __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant
                                                            const int32_t* n_moves,
                                                            const int32_t* newidx, int Hkv,
                                                            int row_bytes, int cap) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x, layer = blockIdx.y;
   const int nm = n_moves[r];
   if (nm == 0) return;
@@ -200,10 +204,9 @@ __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant
 
 int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t s) {
   const trie_cfg& c = h->cfg;
-  k_prune_scan<<<c.n_requests, PRUNE_BS, 0, s>>>(h->token, h->parent, h->depth, h->mask,
-                                                 h->leaf, h->n_nodes, h->n_kv, h->tlen,
-                                                 h->newidx, h->moves, h->n_moves, h->b_live,
-                                                 c.capacity, h->status);
+  launch_k(k_prune_scan, dim3(c.n_requests), dim3(PRUNE_BS), 0, s, h->token, h->parent, h->depth,
+           h->mask, h->leaf, h->n_nodes, (const int32_t*)h->n_kv, (const int32_t*)h->tlen, h->newidx,
+           h->moves, h->n_moves, h->b_live, c.capacity, h->status);
   int rc = trie_check_launch("k_prune_scan");
   if (rc) return rc;
   if (c.n_layers == 0 || kp == nullptr) return TRIE_OK;
@@ -214,8 +217,9 @@ int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t 
   }
   const int esz = c.kv_dtype == TRIE_BF16 ? 2 : 4;
   dim3 grid(c.n_requests, c.n_layers);
-  k_kv_compact<<<grid, COMPACT_BS, 0, s>>>(pp, h->moves, h->n_moves, h->newidx, c.n_kv_heads,
-                                           c.head_dim * esz, c.capacity);
+  launch_k(k_kv_compact, grid, dim3(COMPACT_BS), 0, s, pp, (const int32_t*)h->moves,
+           (const int32_t*)h->n_moves, (const int32_t*)h->newidx, c.n_kv_heads, c.head_dim * esz,
+           c.capacity);
   return trie_check_launch("k_kv_compact");
 }
 

@@ -36,6 +36,9 @@ CASES = [
     ("b32-d64", 1, 32, 300, False, 6, 0.5, 4, 2, 64, 0, "bf16", True),
     ("b12-g4", 2, 12, 400, True, 6, 0.5, 8, 2, 128, 0, "bf16", True),
     ("b1", 3, 1, 40, True, 5, 0.0, 4, 4, 32, 0, "f32", True),
+    # long tries at Qg = 16 / 32 take the tcgen05 kernel by the default plan (>= 1024 rows)
+    ("llama-long-qg32", 1, 8, 1200, True, 12, 0.5, 32, 8, 128, 0, "bf16", True),
+    ("qg16-swa-long", 2, 4, 1100, True, 10, 0.5, 16, 4, 128, 300, "bf16", True),
     ("d256", 1, 2, 70, False, 4, 0.5, 2, 1, 256, 0, "f32", True),
 ]
 
@@ -170,3 +173,23 @@ def test_fused_rope_attention_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W):
         o_ref, lse_ref = attn_ref(qr, Kr[:, :T.N], Vr[:, :T.N], T, window=W)
         assert rel_err(o[r], o_ref) <= 2e-2, f"{name} r={r}: {rel_err(o[r], o_ref)}"
         assert np.abs(l[r] - lse_ref).max() <= 2e-2 * max(1.0, np.abs(lse_ref).max())
+
+
+def test_attention_plan_paths():
+    """The kernel choice the bench relies on: narrow (Qg <= 16, short), wide (Qg 17..32,
+    short tries), tcgen05 (Qg >= 33, or Qg >= 9 at D = 128 with >= 1024 rows)."""
+    need_gpu()
+    from paper_2502_00085_b200 import _lib
+    import os
+    if os.environ.get("TRIE_UMMA_MIN_QG") or os.environ.get("TRIE_ATTN_PERSIST"):
+        pytest.skip("plan overridden by environment")
+
+    def path(b, Hq, Hkv, D, cap, rows):
+        cfg = _lib.make_cfg(2, b, 8, cap, 1, Hq, Hkv, D, 1000, 0, 1, _lib.TRIE_BF16)
+        return _lib.trie_attn_plan_info(cfg, b, rows)["path"]
+    assert path(4, 32, 32, 96, 1088, 864).startswith("narrow")         # Phi, Qg = 4
+    assert path(8, 32, 8, 128, 448, 406).startswith("wide")            # Llama t=150, Qg = 32
+    assert path(8, 32, 8, 128, 8448, 8320).startswith("tcgen05")       # sweep t=8192, Qg = 32
+    assert path(4, 32, 8, 128, 8448, 8320).startswith("tcgen05")       # sweep, Qg = 16
+    assert path(16, 32, 8, 128, 448, 406).startswith("tcgen05")        # Qg = 64
+    assert path(2, 32, 8, 128, 8448, 8320).startswith("narrow")        # Qg = 8
