@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
   // queries held by this thread in the S^T / O^T fragments: columns 2cq, 2cq+1 of each n-tile
   int beam[NQ][2], lod[NQ][2];
   bool qok[NQ][2];
+  uint32_t bbit[NQ][2];  // this query's beam bit (0 for padding queries)
 #pragma unroll
   for (int nq = 0; nq < NQ; ++nq)
 #pragma unroll
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       const int m = nq * 8 + cq * 2 + e;
       qok[nq][e] = m < Qg;
       beam[nq][e] = m < Qg ? m / g : 0;
+      bbit[nq][e] = m < Qg ? 1u << beam[nq][e] : 0u;
       lod[nq][e] = INT_MIN;
       if (p.window > 0 && m < Qg)
         lod[nq][e] = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam[nq][e]]] - p.window + 1;
@@ -240,22 +242,21 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     } else {
       const uint32_t* tmask = (const uint32_t*)(st + 2 * RG::TILE_BYTES);
       const int* tdep = (const int*)(st + 2 * RG::TILE_BYTES + TC_TR * 4);
+      const bool win = p.window > 0;
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {  // fragment rows gq (hh=0) and gq+8 (hh=1)
           const int lr = mt * 16 + gq + hh * 8;
           const int n = n0 + lr;
-          const bool rowin = n < it.N;
-          const uint32_t mw = rowin ? tmask[lr] : 0u;
-          const int dep = rowin ? tdep[lr] : INT_MIN;
-          const bool prompt = n < it.t;
+          // visible-beam word of the row: none past N, all on the prompt (Alg. 3 l.2)
+          const uint32_t vis = n >= it.N ? 0u : (n < it.t ? ~0u : tmask[lr]);
+          const int dep = win ? tdep[lr] : 0;
 #pragma unroll
           for (int nq = 0; nq < NQ; ++nq)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const bool ok = rowin && qok[nq][e] && (prompt || ((mw >> beam[nq][e]) & 1u)) &&
-                              dep >= lod[nq][e];
+              const bool ok = (vis & bbit[nq][e]) != 0u && dep >= lod[nq][e];
               const float v = ok ? sacc[mt][nq][hh * 2 + e] * sc : -INFINITY;
               sacc[mt][nq][hh * 2 + e] = v;
               tmax[nq][e] = fmaxf(tmax[nq][e], v);
@@ -435,27 +436,32 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
   const int gq = lane >> 2, cq = lane & 3;
   const size_t mbase = (size_t)r * p.cap;
   int qm[2], beam[2], lod[2];
+  uint32_t bbit[2];  // this query's beam bit (0 for padding queries)
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     qm[u] = mt * 16 + gq + 8 * u;
     beam[u] = qm[u] < Qg ? qm[u] / g : 0;
+    bbit[u] = qm[u] < Qg ? 1u << beam[u] : 0u;
     lod[u] = INT_MIN;
     if (p.window > 0 && qm[u] < Qg)
       lod[u] = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam[u]]] - p.window + 1;
   }
   uint32_t qa[C::KS][4];
   {
-    const __nv_bfloat16* qb = (const __nv_bfloat16*)p.q;
+    // the two query rows' base pointers (query m = beam j * g + head i of the group)
+    const __nv_bfloat16* qrow[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      qrow[u] = qm[u] < Qg ? (const __nv_bfloat16*)p.q +
+                                 (((size_t)r * p.b_live + beam[u]) * p.Hq + h * g + qm[u] - beam[u] * g) * D
+                           : nullptr;
 #pragma unroll
     for (int ks = 0; ks < C::KS; ++ks)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int row = (u & 1) ? qm[1] : qm[0];
+        const __nv_bfloat16* src = qrow[u & 1];
         const int col = ks * 16 + (u >> 1) * 8 + cq * 2;
-        uint32_t v = 0u;
-        if (row < Qg)
-          v = *(const uint32_t*)(qb + (((size_t)r * p.b_live + row / g) * p.Hq + h * g + row % g) * D + col);
-        qa[ks][u] = v;
+        qa[ks][u] = src ? *(const uint32_t*)(src + col) : 0u;
       }
   }
   float o[C::DT][4];
@@ -502,19 +508,19 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     } else {
       const uint32_t* tmask = (const uint32_t*)(st + 2 * RG::TILE_BYTES);
       const int* tdep = (const int*)(st + 2 * RG::TILE_BYTES + TC_TR * 4);
+      const bool win = p.window > 0;
 #pragma unroll
       for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int lr = r0 + nt * 8 + cq * 2 + cc;
           const int n = n0 + lr;
-          const bool rowin = n < it.N;
-          const uint32_t mw = rowin ? tmask[lr] : 0u;
-          const int dep = rowin ? tdep[lr] : INT_MIN;
-          const bool prompt = n < it.t;
+          // visible-beam word of the row: none past N, all on the prompt (Alg. 3 l.2)
+          const uint32_t vis = n >= it.N ? 0u : (n < it.t ? ~0u : tmask[lr]);
+          const int dep = win ? tdep[lr] : 0;
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const bool ok = rowin && qm[u] < Qg && (prompt || ((mw >> beam[u]) & 1u)) && dep >= lod[u];
+            const bool ok = (vis & bbit[u]) != 0u && dep >= lod[u];
             const float v = ok ? sacc[nt][u * 2 + cc] * sc : -INFINITY;
             sacc[nt][u * 2 + cc] = v;
             tmax[u] = fmaxf(tmax[u], v);

@@ -319,11 +319,14 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
     {  // Q -> smem, 64B-swizzled K-major boxes of [128 rows][32 cols]; padding rows zero
       const __nv_bfloat16* q = (const __nv_bfloat16*)p.q;
       const int chunks = 128 * (D / 8);
+      const float inv_g = 1.f / (float)g;  // exact: m < 128, g <= 128
       for (int c = tid; c < chunks; c += C::NSW * 32) {
         const int m = c / (D / 8), col = (c % (D / 8)) * 8;
         int4 v = make_int4(0, 0, 0, 0);
-        if (m < Qg)
-          v = *(const int4*)(q + (((size_t)r * p.b_live + m / g) * p.Hq + h * g + m % g) * D + col);
+        if (m < Qg) {
+          const int j = __float2int_rz(((float)m + 0.5f) * inv_g);
+          v = *(const int4*)(q + (((size_t)r * p.b_live + j) * p.Hq + h * g + m - j * g) * D + col);
+        }
         const int box = col / TC_CW;
         const uint32_t o = (uint32_t)m * 64u + (uint32_t)(col % TC_CW) * 2u;
         *(int4*)(qsm + box * 128 * 64 + (o ^ (((o >> 7) & 3u) << 4))) = v;
