@@ -171,9 +171,10 @@ class HotPath:
         from paper_2502_00085_b200 import _lib
         self.plan = {var: _lib.trie_attn_plan_info(self.st.cfg, bl, self.rows_hint)
                      for var, bl in (("first", 1), ("steady", b))}
-        # trie_attn_decode_rope (one launch per layer) is opt-in: r07 measured 118.6 us per
-        # fused launch vs 112.7 us for trie_rope_kv_append + trie_attn_decode on Phi
-        self.fused = {var: self.plan[var]["fused_rope"] and os.environ.get("TRIE_BENCH_FUSED") == "1"
+        # a-1 + a-3 as one trie_attn_decode_rope launch per layer wherever the plan has a
+        # fused kernel (narrow / wide): measured r27, request-steps/s fused vs two launches:
+        # Llama 52,301 vs 48,464, Phi 17,309 vs 17,062.  TRIE_BENCH_FUSED=0 forces two launches.
+        self.fused = {var: self.plan[var]["fused_rope"] and os.environ.get("TRIE_BENCH_FUSED") != "0"
                       for var in self.plan}
 
     def step_ops(self, var, slot, events=None):
@@ -190,6 +191,8 @@ class HotPath:
             if fused:  # a-1 + a-3 in one launch
                 st.attn_decode_rope(q, k, v, self.kp[l], self.vp[l], self.wl["theta"], d["out"],
                                     rows_hint=self.rows_hint)
+                if self.gathered is not None:
+                    self._gather(d["out"])
                 continue
             st.rope_kv_append(q, k, v, self.kp[l], self.vp[l], self.wl["theta"])
             if events is not None:
@@ -252,9 +255,14 @@ class HotPath:
             self.replay(0)
         torch.cuda.synchronize()
 
-        def launches():
+        def launches():  # the launch the step makes (fused a-1 + a-3 where planned)
             for l in range(L):
-                st.attn_decode(d["views"][l][0], self.kp[l], self.vp[l], d["out"], rows_hint=self.rows_hint)
+                q, k, v = d["views"][l]
+                if self.fused["steady"]:  # idempotent: q is read, the leaves' rows re-written
+                    st.attn_decode_rope(q, k, v, self.kp[l], self.vp[l], self.wl["theta"], d["out"],
+                                        rows_hint=self.rows_hint)
+                else:
+                    st.attn_decode(q, self.kp[l], self.vp[l], d["out"], rows_hint=self.rows_hint)
         launches()  # warm (scratch sizing)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
@@ -433,6 +441,8 @@ def run_gpu(args):
                            unit="GB/s", frac=round(ach / peak, 4), frac_of_8TBps=round(ach / 8000, 4),
                            traffic=_traffic(args.workload, R, b), peak_source=peak_src,
                            avg_launch_us=round(c_us, 2), bytes_per_launch=int(c_bytes),
+                           kernel_launch=("trie_attn_decode_rope (fused a-1 + a-3; bytes counted: a-3 only)"
+                                          if hp.fused["steady"] else "trie_attn_decode"),
                            timing=(f"CUDA events around a graph of the step's {hp.L} attention launches "
                                    f"(one per layer, back to back, at step {hp.k} of a job), replayed "
                                    f"after the timed steps; achieved = algorithmic bytes / mean launch time"),

@@ -97,41 +97,9 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     } else if (lane == 0) {
       producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
     }
-    if constexpr (ROPE) if (lane != 0) {
-      // lanes 1..31: write-before-read append (§3.4, Alg. 3 l.7) of the leaves whose slots
-      // lie in this CTA's tiles -- K rotated at the beam's depth with the step's (cos, sin)
-      // table, V copied -- then fence the generic writes for the TMA (async proxy) reads
-      // of lane 0, which waits on app_done only before the tile holding the first leaf.
-      const size_t mb = (size_t)r * p.cap;
-      (void)mb;
-      const int slot_lo = it.tile0 * TC_TR, slot_hi = (it.tile0 + it.ntiles) * TC_TR;
-      const __nv_bfloat16* kn = (const __nv_bfloat16*)p.k_new;
-      const __nv_bfloat16* vn = (const __nv_bfloat16*)p.v_new;
-      __nv_bfloat16* kpool = (__nv_bfloat16*)p.k;
-      __nv_bfloat16* vpool = (__nv_bfloat16*)p.v;
-      constexpr int HALF = D / 2;
-      for (int e = lane - 1; e < p.b_live * HALF; e += 31) {
-        const int j = e / HALF, i = e % HALF;
-        const int slot = p.leaf[r * TRIE_MAX_BEAMS + j];
-        if (slot < slot_lo || slot >= slot_hi) continue;
-        const __nv_bfloat16* src = kn + (((size_t)r * p.b_live + j) * p.Hkv + h) * D;
-        const float x1 = __bfloat162float(src[i]), x2 = __bfloat162float(src[i + HALF]);
-        const float2 c = p.rope_tab[((size_t)r * p.b_live + j) * HALF + i];
-        __nv_bfloat16* dst = kpool + (((size_t)r * p.Hkv + h) * p.cap + slot) * D;
-        dst[i] = __float2bfloat16_rn(x1 * c.x - x2 * c.y);
-        dst[i + HALF] = __float2bfloat16_rn(x2 * c.x + x1 * c.y);
-      }
-      for (int e = lane - 1; e < p.b_live * (D / 8); e += 31) {  // 16-byte V copies
-        const int j = e / (D / 8), d = (e % (D / 8)) * 8;
-        const int slot = p.leaf[r * TRIE_MAX_BEAMS + j];
-        if (slot < slot_lo || slot >= slot_hi) continue;
-        *(int4*)(vpool + (((size_t)r * p.Hkv + h) * p.cap + slot) * D + d) =
-            *(const int4*)(vn + (((size_t)r * p.b_live + j) * p.Hkv + h) * D + d);
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      __syncwarp(0xfffffffeu);
-      if (lane == 1) mbar_arrive(app_done);
-    }
+    if constexpr (ROPE) if (lane != 0)
+      append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane, app_done,
+                            it.N - p.b_live);
     return;
   }
   // ===== consumer warp =====
@@ -398,7 +366,10 @@ struct WideCfg {
 // Warp (mt, rs) owns query m-tile mt (16 queries) and rows [rs*RSZ, (rs+1)*RSZ) of every
 // tile; with RS > 1 the row slices of an m-tile are merged once, at the end, through the
 // (drained) ring.  S = Q K^T with two independent n-tiles per ldmatrix.x4.
-template <int D, int MT, int RS>
+// ROPE: fused a-1 (trie_attn_decode_rope) -- Q is read un-rotated and rotated in registers
+// (the rotate-half partner of column c < D/2 is column c + D/2, held by the same thread
+// in k-step ks + KS/2), the leaves' K/V rows are appended by the producer warp's idle lanes.
+template <int D, int MT, int RS, bool ROPE = false>
 __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p) {
@@ -409,7 +380,8 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
   uint8_t* ring = smem;
   uint64_t* full = (uint64_t*)(smem + RG::RING_BYTES);
   uint64_t* empty = full + C::STAGES;
-  ItemInfo* info = (ItemInfo*)(empty + C::STAGES);
+  uint64_t* app_done = empty + C::STAGES;
+  ItemInfo* info = (ItemInfo*)(app_done + 1);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
   pdl_trigger();
@@ -419,6 +391,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NC);
     }
+    mbar_init(app_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();  // the shared-memory setup above ran before the predecessor finished
@@ -426,7 +399,23 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
   __syncthreads();
   const ItemInfo it = *info;
   if (warp == 0) {
-    if (lane == 0) producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+    if constexpr (ROPE) {  // as in k_attn_narrow: leaf-free tiles first, then the rest
+      const int first_leaf = it.N - p.b_live;
+      int fill = min(C::STAGES, it.ntiles);
+      while (fill > 0 && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
+      if (lane == 0)
+        producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr,
+                                    INT_MAX, 0, fill);
+      __syncwarp();
+      if (lane == 0)
+        producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
+                                    first_leaf, fill);
+      else
+        append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane,
+                              app_done, first_leaf);
+    } else if (lane == 0) {
+      producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+    }
     return;
   }
   const int cw = warp - 1;
@@ -463,6 +452,22 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
         const int col = ks * 16 + (u >> 1) * 8 + cq * 2;
         qa[ks][u] = src ? *(const uint32_t*)(src + col) : 0u;
       }
+    if constexpr (ROPE) {  // rotate-half at the beam's depth, rounded to bf16 like a-1
+      constexpr int HALF = D / 2;
+#pragma unroll
+      for (int ks = 0; ks < C::KS / 2; ++ks)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (!qrow[u & 1]) continue;
+          const int col = ks * 16 + (u >> 1) * 8 + cq * 2;  // < HALF; partner col + HALF
+          const float4 t = __ldg((const float4*)(p.rope_tab +
+                                                 ((size_t)r * p.b_live + beam[u & 1]) * HALF + col));
+          const float2 x1 = __bfloat1622float2(*(const __nv_bfloat162*)&qa[ks][u]);
+          const float2 x2 = __bfloat1622float2(*(const __nv_bfloat162*)&qa[ks + C::KS / 2][u]);
+          qa[ks][u] = pack_bf16(x1.x * t.x - x2.x * t.y, x1.y * t.z - x2.y * t.w);
+          qa[ks + C::KS / 2][u] = pack_bf16(x2.x * t.x + x1.x * t.y, x2.y * t.z + x1.y * t.w);
+        }
+    }
   }
   float o[C::DT][4];
 #pragma unroll
@@ -732,10 +737,10 @@ static const TcKernel& narrow_k() {
       make_tc(k_attn_narrow<D, NQ, ST, ROPE>, NarrowCfg<D, NQ, ST, ROPE>::SMEM, 64);
   return k;
 }
-template <int D, int MT, int RS>
+template <int D, int MT, int RS, bool ROPE = false>
 static const TcKernel& wide_k() {
-  static const TcKernel k =
-      make_tc(k_attn_wide<D, MT, RS>, WideCfg<D, MT, RS>::SMEM, WideCfg<D, MT, RS>::THREADS);
+  static const TcKernel k = make_tc(k_attn_wide<D, MT, RS, ROPE>, WideCfg<D, MT, RS>::SMEM,
+                                    WideCfg<D, MT, RS>::THREADS);
   return k;
 }
 // row slices per wide tile (TRIE_WIDE_RS in {1, 2, 4}; default 2: two warps per query
@@ -749,12 +754,12 @@ static int wide_rs() {
   }
   return v;
 }
-template <int D, int MT>
+template <int D, int MT, bool ROPE = false>
 static const TcKernel& wide_sel() {
   switch (wide_rs()) {
-    case 1: return wide_k<D, MT, 1>();
-    case 4: return wide_k<D, MT, (MT <= 2 ? 4 : 2)>();
-    default: return wide_k<D, MT, (MT <= 4 ? 2 : 1)>();
+    case 1: return wide_k<D, MT, 1, ROPE>();
+    case 4: return wide_k<D, MT, (MT <= 2 ? 4 : 2), ROPE>();
+    default: return wide_k<D, MT, (MT <= 4 ? 2 : 1), ROPE>();
   }
 }
 
@@ -783,7 +788,7 @@ template <int D>
 static const TcKernel& select_d(int Qg, bool rope) {
   if (Qg <= 8) return rope ? narrow_sel<D, 1, true>() : narrow_sel<D, 1, false>();
   if (Qg <= 16) return rope ? narrow_sel<D, 2, true>() : narrow_sel<D, 2, false>();
-  if (Qg <= 32) return wide_sel<D, 2>();
+  if (Qg <= 32) return rope ? wide_sel<D, 2, true>() : wide_sel<D, 2, false>();
   if (Qg <= 64) return wide_sel<D, 4>();
   return wide_sel<D, 8>();
 }
@@ -796,10 +801,10 @@ static const TcKernel* select_tc(int D, int Qg, bool rope = false) {
   return nullptr;
 }
 
-// The fused RoPE + append variant exists for the narrow kernel (Qg <= 16).
+// The fused RoPE + append variants: narrow (Qg <= 16) and wide at Qg <= 32.
 bool attn_rope_fusable(const AttnParams& p) {
   const int Qg = p.b_live * (p.Hq / p.Hkv);
-  return attn_tc_supported(p) && !attn_umma_eligible(p) && Qg <= 16;
+  return attn_tc_supported(p) && !attn_umma_eligible(p) && Qg <= 32;
 }
 
 bool attn_tc_shape_ok(const AttnParams& p) {

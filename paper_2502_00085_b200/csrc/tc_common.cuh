@@ -164,6 +164,61 @@ __device__ __forceinline__ void item_setup(const AttnParams& p, int r, int split
   }
 }
 
+// Fused a-1 (trie_attn_decode_rope): lanes 1..31 of the producer warp append the leaves
+// whose slots lie in [slot_lo, slot_hi) -- K rotated at the beam's depth with the step's
+// (cos, sin) table, V copied, 8-element chunks with all loads of an item issued together
+// (write-before-read, §3.4 / Alg. 3 l.7) -- then fence the generic writes for the TMA
+// (async proxy) reads of lane 0, which waits on app_done before the tile of the first leaf.
+// The leaves are the last b_live slots (invariant 2 of the handle's trie: appends go to
+// the end, compaction is stable), so leaf j's slot is first_leaf + j -- no load of leaf[].
+template <int D>
+__device__ __forceinline__ void append_leaves_rope(const AttnParams& p, int r, int h, int slot_lo,
+                                                   int slot_hi, int lane, uint64_t* app_done,
+                                                   int first_leaf) {
+  constexpr int HALF = D / 2, CH = HALF / 8;
+  static_assert(HALF % 8 == 0, "head_dim must be a multiple of 16");
+  const __nv_bfloat16* __restrict__ kn = (const __nv_bfloat16*)p.k_new;
+  const __nv_bfloat16* __restrict__ vn = (const __nv_bfloat16*)p.v_new;
+  __nv_bfloat16* kpool = (__nv_bfloat16*)p.k;
+  __nv_bfloat16* vpool = (__nv_bfloat16*)p.v;
+  const int nk = p.b_live * CH, nv = p.b_live * (D / 8);
+  for (int e = lane - 1; e < nk + nv; e += 31) {
+    const int j = e < nk ? e / CH : (e - nk) / (D / 8);
+    const int slot = first_leaf + j;
+    if (slot < slot_lo || slot >= slot_hi) continue;
+    const size_t rj = (size_t)r * p.b_live + j;
+    __nv_bfloat16* dst = (e < nk ? kpool : vpool) + (((size_t)r * p.Hkv + h) * p.cap + slot) * D;
+    if (e < nk) {
+      const int c = (e % CH) * 8;
+      const __nv_bfloat16* src = kn + (rj * p.Hkv + h) * D;
+      const int4 a = __ldg((const int4*)(src + c)), b = __ldg((const int4*)(src + HALF + c));
+      const float4* tb = (const float4*)(p.rope_tab + rj * HALF + c);  // 8 (cos, sin) pairs
+      float4 t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] = __ldg(tb + u);
+      const __nv_bfloat162* a2 = (const __nv_bfloat162*)&a;
+      const __nv_bfloat162* b2 = (const __nv_bfloat162*)&b;
+      int4 y1, y2;
+      __nv_bfloat162* o1 = (__nv_bfloat162*)&y1;
+      __nv_bfloat162* o2 = (__nv_bfloat162*)&y2;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // elements 2u, 2u + 1: table pairs t[u].(x,y), t[u].(z,w)
+        const float2 x1 = __bfloat1622float2(a2[u]), x2 = __bfloat1622float2(b2[u]);
+        o1[u] = __floats2bfloat162_rn(x1.x * t[u].x - x2.x * t[u].y, x1.y * t[u].z - x2.y * t[u].w);
+        o2[u] = __floats2bfloat162_rn(x2.x * t[u].x + x1.x * t[u].y, x2.y * t[u].z + x1.y * t[u].w);
+      }
+      *(int4*)(dst + c) = y1;
+      *(int4*)(dst + HALF + c) = y2;
+    } else {
+      const int d = ((e - nk) % (D / 8)) * 8;
+      *(int4*)(dst + d) = __ldg((const int4*)(vn + (rj * p.Hkv + h) * D + d));
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncwarp(0xfffffffeu);
+  if (lane == 1) mbar_arrive(app_done);
+}
+
 template <int D, int STAGES>
 __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUtensorMap* vmap,
                                               const AttnParams& p, int r, int h,

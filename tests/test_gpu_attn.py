@@ -122,7 +122,10 @@ def test_rope_kv_append_matches_oracle(dt):
     ("gqa-fused", 2, 4, 200, 8, 2, 128, 0),
     ("swa-fused", 1, 4, 150, 4, 1, 64, 40),
     ("split-fused", 1, 2, 1500, 2, 2, 128, 0),
-    ("wide-unfused", 1, 8, 130, 8, 2, 128, 0),   # Qg = 32: two-launch fallback
+    ("wide-fused", 1, 8, 130, 8, 2, 128, 0),      # Qg = 32: wide kernel, fused
+    ("wide-fused-llama", 2, 8, 150, 32, 8, 128, 0),
+    ("wide-fused-split", 1, 6, 1000, 16, 4, 64, 0),  # Qg = 24, D = 64, split K
+    ("umma-unfused", 1, 16, 130, 8, 2, 128, 0),   # Qg = 64: tcgen05, two-launch fallback
 ])
 def test_fused_rope_attention_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W):
     """trie_attn_decode_rope == RoPE at depth (§3.4) + write-before-read append + trie
