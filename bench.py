@@ -165,6 +165,7 @@ class HotPath:
         self.sel_t = torch.empty_like(self.sel_p)
         self.sel_s = torch.empty(R, b, dtype=torch.float32, device=dev)
         self.rows_hint = t + s
+        self.g = int(wl.get("g", 1))  # GC interval (Alg. 2); 1 on the hot path
         self.graphs = {}
         self.launches_per_graph = {}
         self.k = 0  # steps done in the current job
@@ -177,8 +178,9 @@ class HotPath:
         self.fused = {var: self.plan[var]["fused_rope"] and os.environ.get("TRIE_BENCH_FUSED") != "0"
                       for var in self.plan}
 
-    def step_ops(self, var, slot, events=None):
-        """Enqueue one step (all §8(a) rows) on the current stream."""
+    def step_ops(self, var, slot, events=None, gc=True):
+        """Enqueue one step (all §8(a) rows) on the current stream; `gc` = run a-6 after
+        the append (Alg. 2 l.5-7 with interval g: the bench's gc_now())."""
         st, L = self.st, self.L
         d = self.inp[(var, slot)]
         if var == "first":
@@ -205,7 +207,8 @@ class HotPath:
         if events is not None and fused:
             events[0][1].record()
         st.beam_step(d["logits"], self.sel_p, self.sel_t, self.sel_s)
-        st.prune_compact(self.kp, self.vp)
+        if gc:
+            st.prune_compact(self.kp, self.vp)
 
     def _gather(self, out):
         from paper_2502_00085_b200.dist import gather_heads
@@ -217,33 +220,43 @@ class HotPath:
         torch = self.torch
         from paper_2502_00085_b200 import _lib
         self.ev = {}
+        gcs = (True,) if self.g == 1 else (True, False)
         for var in ("first", "steady"):
             for slot in range(self.NB):
-                for timed in (False, True):
-                    evs = None
-                    if timed:
-                        n_pairs = 1 if self.fused[var] else self.L
-                        evs = [(torch.cuda.Event(enable_timing=True, external=True),
-                                torch.cuda.Event(enable_timing=True, external=True)) for _ in range(n_pairs)]
-                    g = torch.cuda.CUDAGraph()
-                    n0 = _lib.trie_launch_count()
-                    with torch.cuda.graph(g):
-                        self.step_ops(var, slot, evs)
-                    self.graphs[(var, slot, timed)] = g
-                    self.launches_per_graph[(var, slot, timed)] = _lib.trie_launch_count() - n0
-                    if timed:
-                        self.ev[(var, slot)] = evs
+                for gc in gcs:
+                    for timed in (False, True):
+                        evs = None
+                        if timed:
+                            n_pairs = 1 if self.fused[var] else self.L
+                            evs = [(torch.cuda.Event(enable_timing=True, external=True),
+                                    torch.cuda.Event(enable_timing=True, external=True))
+                                   for _ in range(n_pairs)]
+                        g = torch.cuda.CUDAGraph()
+                        n0 = _lib.trie_launch_count()
+                        with torch.cuda.graph(g):
+                            self.step_ops(var, slot, evs, gc)
+                        key = ((var, gc), slot, timed)
+                        self.graphs[key] = g
+                        self.launches_per_graph[key] = _lib.trie_launch_count() - n0
+                        if timed:
+                            self.ev[((var, gc), slot)] = evs
         # capture ran the host logic of reset/beam_step: leave the host view at "steady"
+
+    def gc_now(self, k=None):
+        """GC after the append of job step k (0-based) iff Alg. 2's top-of-iteration test
+        i mod g == 0 holds at i = t + k + 1 (readings R7 / R8); g = 0: never."""
+        k = self.k if k is None else k
+        return self.g == 1 or (self.g > 1 and (self.t + k + 1) % self.g == 0)
 
     def next_key(self):
         var = "first" if self.k % self.s == 0 else "steady"
-        return var
+        return (var, self.gc_now())
 
     def replay(self, slot, timed=False):
-        var = self.next_key()
-        self.graphs[(var, slot, timed)].replay()
+        key = self.next_key()
+        self.graphs[(key, slot, timed)].replay()
         self.k = (self.k + 1) % self.s
-        return var
+        return key
 
     def attn_only_timing(self, reps=10):
         """Mean duration (us) and algorithmic bytes of one trie_attn_decode launch: a graph
@@ -276,7 +289,18 @@ class HotPath:
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / (reps * L)
-        return us, self.attn_bytes(self.k, st.n_nodes.cpu().numpy())
+        return us, self.attn_bytes(self.k, self.live_rows())
+
+    def live_rows(self):
+        """Per request: rows some live beam can see (prompt + generated nodes with a
+        beam bit).  With GC every step this is N; with g > 1 dead rows (mask 0) are not
+        algorithmic bytes although the kernel still streams them."""
+        N = self.st.n_nodes.cpu().numpy()
+        if self.g == 1:
+            return N
+        m = self.st.beam_mask.cpu().numpy()
+        t = self.st.prompt_len.cpu().numpy()
+        return np.array([t[r] + int(np.count_nonzero(m[r, t[r]:N[r]])) for r in range(self.R)])
 
     def attn_bytes(self, k_in_job, N):
         """Algorithmic bytes of one trie_attn_decode launch: unique
@@ -322,6 +346,7 @@ def run_gpu(args):
         wl["b"] = args.beam
     if args.requests:
         wl["R"] = args.requests
+    wl["g"] = args.gc_interval
     if wl.get("kv_shard") and world > 1 and backend != "nccl":
         raise SystemExit("the KV-head shard's per-layer all-gather is captured in CUDA graphs: NCCL only")
     hp = HotPath(wl, rank, dev, world)
@@ -329,7 +354,7 @@ def run_gpu(args):
 
     # eager warm-up (allocates scratch, sets kernel attributes), then capture
     for i in range(2):
-        hp.step_ops("first" if i == 0 else "steady", i % 2)
+        hp.step_ops("first" if i == 0 else "steady", i % 2, gc=hp.gc_now(i))
     torch.cuda.synchronize()
     hp.capture()
     hp.st.reset()
@@ -361,7 +386,7 @@ def run_gpu(args):
     def harvest(slot):
         var_p, kj_p, i_p = pending.pop(slot)
         end_ev[slot].synchronize()  # only step i_p; step i_p + 1 keeps the GPU busy
-        evs = hp.ev[(var_p, slot)]
+        evs = hp.ev[(var_p, slot)]  # var_p = (variant, gc) key
         per = hp.L // len(evs)  # fused: one pair spans the L attention launches of the step
         for e0, e1 in evs:
             dt = e0.elapsed_time(e1)
@@ -430,7 +455,7 @@ def run_gpu(args):
                config=dict(workload=wl["name"], requests_per_gpu=R, beam=b, prompt_len=t,
                            new_tokens=s, layers=L, q_heads_per_gpu=hp.Hq, kv_heads_per_gpu=hp.Hkv,
                            head_dim=hp.D,
-                           vocab=hp.V, window=hp.W, gc_interval=1,
+                           vocab=hp.V, window=hp.W, gc_interval=hp.g,
                            parallelism=(f"kv-head-shard{world} (per-layer all-gather of attention outputs)"
                                         if hp.kv_shard else f"request-dp{world}"),
                            execution="cuda-graph replay per step",
@@ -464,6 +489,7 @@ def run_gpu(args):
     # batch beam search keeps b*(t+k) rows per request (prompt replicated, pending token
     # included: the paper's 21 = 3 x 7 counting); the trie keeps N rows
     res["kv_memory"] = dict(step_in_job=int(k_star), trie_bytes=trie_b, batch_bytes=batch_b,
+                            trie_peak_bytes=int(nh.sum(axis=1).max()) * kv_row,
                             ratio_batch_over_trie=round(batch_b / max(trie_b, 1), 3),
                             bound_b_ts_over_t_s_b_1=round(b * (t + k_star) / (t + k_star + b - 1), 3))
     if not args.no_e2e:
@@ -639,6 +665,8 @@ def main():
     ap.add_argument("--workload", default="phi", choices=sorted(WORKLOADS))
     ap.add_argument("--beam", type=int, default=0)
     ap.add_argument("--requests", type=int, default=0)
+    ap.add_argument("--gc-interval", type=int, default=1,
+                    help="Alg. 2's GC interval g (1 = every step, the hot path; 0 = never)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
