@@ -13,7 +13,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtriedecode.so")
+# TRIE_LIB: an alternative build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("TRIE_LIB") or os.path.join(_HERE, "libtriedecode.so")
 
 TRIE_F32, TRIE_BF16 = 0, 1
 TRIE_ST_CAPACITY, TRIE_ST_PARENT, TRIE_ST_EMPTY_ROW, TRIE_ST_LEAF = 1, 2, 4, 8

@@ -12,7 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libtriedecode.so")
+# TRIE_BUILD_OUT: write an alternative build elsewhere (A/B experiments, see _lib.TRIE_LIB)
+LIB = os.environ.get("TRIE_BUILD_OUT") or os.path.join(HERE, "libtriedecode.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -23,7 +24,7 @@ FLAGS = [
 ]
 # experiment builds: TRIE_BUILD_DEFINES="TRIE_UMMA_TRACE=1" (use --force; see scripts/umma_trace.py)
 FLAGS += ["-D" + d for d in os.environ.get("TRIE_BUILD_DEFINES", "").split() if d]
-OBJDIR = os.path.join(HERE, "build_obj")
+OBJDIR = os.path.join(HERE, "build_obj" + ("_alt" if os.environ.get("TRIE_BUILD_OUT") else ""))
 
 
 def sources():

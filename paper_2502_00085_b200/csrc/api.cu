@@ -61,6 +61,16 @@ bool trie::pdl_enabled() {
   return v == 1;
 }
 
+// pre-wait prefetch of prompt tiles in the fused attention (TRIE_PREFETCH=0 disables)
+static bool prefetch_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TRIE_PREFETCH");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
@@ -413,6 +423,12 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.aux = scratch;
   p.part = (float*)((char*)scratch + pl.counter_bytes);
   p.splits = pl.splits;
+  if (cfg->window == 0 && pl.splits == 1 && prefetch_enabled()) {
+    // tiles below the shortest prompt are prompt rows in every request (AttnParams::pre_tiles)
+    int t_min = INT32_MAX;
+    for (int32_t t : h->host_tlen) t_min = t < t_min ? t : t_min;
+    p.pre_tiles = t_min / 64;
+  }
   return trie::launch_attn_tc(p, stream);
 }
 

@@ -28,6 +28,12 @@ struct AttnParams {
   const void* k_new;      // [R][b_live][Hkv][D]
   const void* v_new;      // [R][b_live][Hkv][D]
   const float2* rope_tab; // [R][b_live][D/2] (cos, sin) of the leaves' depths (per step)
+  // pre_tiles > 0: the first pre_tiles 64-slot tiles of every request hold prompt rows
+  // only (host-known minimum prompt length, no window, one split).  Those rows are written
+  // by the caller's prefill before trie_create / trie_reset and never again by any kernel
+  // of the library (the prompt never moves, invariant 3), so their K/V may be loaded
+  // BEFORE griddepcontrol.wait: the first ring stages fill while the predecessor drains.
+  int pre_tiles;
 };
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);

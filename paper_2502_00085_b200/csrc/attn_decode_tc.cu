@@ -34,6 +34,23 @@
 
 namespace trie {
 
+// Experiment build only (TRIE_BUILD_DEFINES="TRIE_ATTN_TRACE=1", scripts/attn_trace.py):
+// %globaltimer stamps per CTA of the narrow / wide kernels -- [0] start, [1] setup done,
+// [2] first tile seen by consumer warp 0, [3] last tile done, [4] epilogue done, [5] the
+// producer issued its last tile, [6] smid, [7] tiles.  Results are still written.
+#ifdef TRIE_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[8 * 65536];
+__device__ __forceinline__ void attn_trc(int k, unsigned long long v = 0) {
+  const size_t cta = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (cta >= 65536) return;
+  if (k != 6 && k != 7) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  g_attn_trace[cta * 8 + k] = v;
+}
+#define ATTN_TRC(cond, k, ...) do { if (cond) attn_trc(k, ##__VA_ARGS__); } while (0)
+#else
+#define ATTN_TRC(cond, k, ...) do { } while (0)
+#endif
+
 // =========================================================================================
 // narrow: Qg <= 8 * NQ (NQ in {1, 2}); CTA = producer warp + one consumer warp
 // =========================================================================================
@@ -67,6 +84,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
   pdl_trigger();
+  ATTN_TRC(threadIdx.x == 0, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -76,33 +94,55 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     mbar_init(app_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // prompt-only tiles loaded before the wait (see AttnParams::pre_tiles)
+  const int npre = min(p.pre_tiles, C::STAGES);
+  if (threadIdx.x == 0 && npre > 0)
+    prefetch_prompt_tiles<D, C::STAGES>(&kmap, &vmap, p, r, h, ring, full, npre);
   pdl_wait();  // the shared-memory setup above ran before the predecessor finished
-  if (threadIdx.x < 32) item_setup(p, r, split, info);
-  __syncthreads();
-  const ItemInfo it = *info;
   if (warp == 0) {
+    // item setup, published to the consumers by a named barrier: they load (and rotate)
+    // their queries meanwhile instead of waiting for it
+    item_setup(p, r, split, info);
+    __syncwarp();
+    const ItemInfo it = *info;
+    __threadfence_block();
+    asm volatile("bar.arrive 2, %0;" ::"r"(64) : "memory");
+#ifdef TRIE_ATTN_TRACE
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      attn_trc(1);
+      attn_trc(6, smid);
+      attn_trc(7, (unsigned long long)it.ntiles);
+    }
+#endif
     if constexpr (ROPE) {
       // fill the ring first (tiles that hold no leaf), then lane 0 streams the rest while
       // lanes 1..31 append the leaves' K/V rows
       const int first_leaf = it.N - p.b_live;
       int fill = min(C::STAGES, it.ntiles);
-      while (fill > 0 && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
+      while (fill > npre && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr,
-                                    INT_MAX, 0, fill);
+                                    INT_MAX, npre, fill);
       __syncwarp();
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
-                                    first_leaf, fill);
+                                    first_leaf, max(fill, npre));
     } else if (lane == 0) {
-      producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+      producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr, INT_MAX,
+                                  npre);
     }
     if constexpr (ROPE) if (lane != 0)
       append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane, app_done,
                             it.N - p.b_live);
+    ATTN_TRC(lane == 0, 5);
     return;
   }
   // ===== consumer warp =====
+  // Waits for the item setup BEFORE loading Q: overlapping the two (as k_attn_wide does)
+  // measured 4.5% slower on the Phi workload (r34 A/B, 16.01k vs 16.76k request-steps/s).
+  asm volatile("bar.sync 2, 64;" ::: "memory");  // item setup published by warp 0
   const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
   const int gq = lane >> 2, cq = lane & 3;
   const size_t mbase = (size_t)r * p.cap;
@@ -157,6 +197,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       }
     }
   }
+  const ItemInfo it = *info;
   float o[C::DM][NQ][4];
 #pragma unroll
   for (int dm = 0; dm < C::DM; ++dm)
@@ -171,6 +212,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
   for (int i = 0; i < it.ntiles; ++i) {
     const int s = i % C::STAGES;
     mbar_wait(&full[s], (uint32_t)(i / C::STAGES) & 1u);
+    ATTN_TRC(i == 0 && lane == 0, 2);
     const uint8_t* st = ring + s * RG::STAGE_BYTES;
     const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + RG::TILE_BYTES);
     const int tile = it.tile0 + i;
@@ -286,6 +328,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  ATTN_TRC(lane == 0, 3);
   // ---- epilogue: column sums over the 8 lanes of a column quad, transpose via smem ----
 #pragma unroll
   for (int nq = 0; nq < NQ; ++nq)
@@ -343,6 +386,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       }
     }
   }
+  ATTN_TRC(lane == 0, 4);
 }
 
 // =========================================================================================
@@ -385,6 +429,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
   pdl_trigger();
+  ATTN_TRC(threadIdx.x == 0, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -394,28 +439,47 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     mbar_init(app_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // prompt-only tiles loaded before the wait (see AttnParams::pre_tiles)
+  const int npre = min(p.pre_tiles, C::STAGES);
+  if (threadIdx.x == 0 && npre > 0)
+    prefetch_prompt_tiles<D, C::STAGES>(&kmap, &vmap, p, r, h, ring, full, npre);
   pdl_wait();  // the shared-memory setup above ran before the predecessor finished
-  if (threadIdx.x < 32) item_setup(p, r, split, info);
-  __syncthreads();
-  const ItemInfo it = *info;
   if (warp == 0) {
+    // item setup, published to the consumers by a named barrier: they load (and rotate)
+    // their queries meanwhile instead of waiting for it
+    item_setup(p, r, split, info);
+    __syncwarp();
+    const ItemInfo it = *info;
+    __threadfence_block();
+    asm volatile("bar.arrive 2, %0;" ::"r"(C::THREADS) : "memory");
+#ifdef TRIE_ATTN_TRACE
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      attn_trc(1);
+      attn_trc(6, smid);
+      attn_trc(7, (unsigned long long)it.ntiles);
+    }
+#endif
     if constexpr (ROPE) {  // as in k_attn_narrow: leaf-free tiles first, then the rest
       const int first_leaf = it.N - p.b_live;
       int fill = min(C::STAGES, it.ntiles);
-      while (fill > 0 && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
+      while (fill > npre && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr,
-                                    INT_MAX, 0, fill);
+                                    INT_MAX, npre, fill);
       __syncwarp();
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
-                                    first_leaf, fill);
+                                    first_leaf, max(fill, npre));
       else
         append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane,
                               app_done, first_leaf);
     } else if (lane == 0) {
-      producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty);
+      producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr, INT_MAX,
+                                  npre);
     }
+    ATTN_TRC(lane == 0, 5);
     return;
   }
   const int cw = warp - 1;
@@ -469,6 +533,10 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
         }
     }
   }
+  // item setup published by warp 0 (the queries were loaded and rotated meanwhile: r34 A/B
+  // on Llama, 58.4k vs 57.4k request-steps/s)
+  asm volatile("bar.sync 2, %0;" ::"r"(C::THREADS) : "memory");
+  const ItemInfo it = *info;
   float o[C::DT][4];
 #pragma unroll
   for (int i = 0; i < C::DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -479,6 +547,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
   for (int i = 0; i < it.ntiles; ++i) {
     const int s = i % C::STAGES;
     mbar_wait(&full[s], (uint32_t)(i / C::STAGES) & 1u);
+    ATTN_TRC(i == 0 && cw == 0 && lane == 0, 2);
     const uint8_t* st = ring + s * RG::STAGE_BYTES;
     const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + RG::TILE_BYTES);
     const int tile = it.tile0 + i;
@@ -579,6 +648,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  ATTN_TRC(cw == 0 && lane == 0, 3);
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     lrow[u] += __shfl_xor_sync(0xffffffffu, lrow[u], 1);
@@ -659,6 +729,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       }
     }
   }
+  ATTN_TRC(cw == 0 && lane == 0, 4);
 }
 
 // ---- host side ---------------------------------------------------------------------------
@@ -858,3 +929,13 @@ int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
 }
 
 }  // namespace trie
+
+#ifdef TRIE_ATTN_TRACE
+// trace build only: copy n CTA records (8 x u64 each) of the last traced launch, then clear
+extern "C" int trie_debug_attn_trace(unsigned long long* host, int n) {
+  if (cudaMemcpyFromSymbol(host, trie::g_attn_trace, (size_t)n * 8 * 8) != cudaSuccess) return -1;
+  void* dev = nullptr;
+  if (cudaGetSymbolAddress(&dev, trie::g_attn_trace) != cudaSuccess) return -1;
+  return cudaMemset(dev, 0, sizeof(trie::g_attn_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif

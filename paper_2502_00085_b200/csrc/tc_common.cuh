@@ -219,6 +219,28 @@ __device__ __forceinline__ void append_leaves_rope(const AttnParams& p, int r, i
   if (lane == 1) mbar_arrive(app_done);
 }
 
+// Pre-wait prefetch (thread 0 = the producer lane, barriers initialised): K/V of the
+// request's first n <= STAGES prompt-only tiles into ring stages 0..n-1 (no mask/depth
+// words: those tiles take the unmasked path); the producer loop then starts at tile n.
+template <int D, int STAGES>
+__device__ __forceinline__ void prefetch_prompt_tiles(const CUtensorMap* kmap,
+                                                      const CUtensorMap* vmap,
+                                                      const AttnParams& p, int r, int h,
+                                                      uint8_t* ring, uint64_t* full, int n) {
+  using RG = Ring<D, STAGES>;
+  const int row_base = (r * p.Hkv + h) * p.cap;
+  for (int i = 0; i < n; ++i) {
+    const uint32_t st = smem_u32(ring + i * RG::STAGE_BYTES);
+    mbar_expect_tx(&full[i], 2 * RG::TILE_BYTES);
+#pragma unroll
+    for (int bx = 0; bx < D / TC_CW; ++bx) {
+      tma_load_2d(st + bx * TC_TR * 64, kmap, bx * TC_CW, row_base + i * TC_TR, &full[i]);
+      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vmap, bx * TC_CW, row_base + i * TC_TR,
+                  &full[i]);
+    }
+  }
+}
+
 template <int D, int STAGES>
 __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUtensorMap* vmap,
                                               const AttnParams& p, int r, int h,

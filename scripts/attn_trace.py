@@ -1,0 +1,85 @@
+"""Experiment: per-CTA %globaltimer timeline of one narrow / wide attention launch
+(trace build only).
+    TRIE_BUILD_DEFINES="TRIE_ATTN_TRACE=1" python -m paper_2502_00085_b200.build --force
+    python scripts/attn_trace.py --workload llama --step 131
+Prints, over the launch's CTAs, the distribution (us, relative to the first CTA start) of:
+start, setup done, first tile seen, last tile done, epilogue done, producer done."""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="llama")
+    ap.add_argument("--step", type=int, default=131)
+    ap.add_argument("--beam", type=int, default=0)
+    ap.add_argument("--requests", type=int, default=0)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    from paper_2502_00085_b200 import _lib
+    lib = _lib.load()
+    fn = lib.trie_debug_attn_trace
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+    wl = dict(bench.WORKLOADS[a.workload])
+    if a.beam:
+        wl["b"] = a.beam
+    if a.requests:
+        wl["R"] = a.requests
+    hp = bench.HotPath(wl, 0, torch.device("cuda", 0))
+    hp.capture()
+    for _ in range(a.step):
+        hp.replay(0)
+    torch.cuda.synchronize()
+    st, d = hp.st, hp.inp[("steady", 0)]
+    q, k, v = d["views"][0]
+    n = hp.R * hp.Hkv * max(1, hp.plan["steady"]["splits"])
+    buf = (ctypes.c_ulonglong * (8 * n))()
+    for rep in range(3):
+        if rep == 2:
+            assert fn(buf, n) == 0  # clears the trace
+        for l in (0, 1):  # the second launch runs right behind the first (PDL overlap)
+            if hp.fused["steady"]:
+                st.attn_decode_rope(q, k, v, hp.kp[l], hp.vp[l], wl["theta"], d["out"], rows_hint=hp.rows_hint)
+            else:
+                st.attn_decode(q, hp.kp[l], hp.vp[l], d["out"], rows_hint=hp.rows_hint)
+        torch.cuda.synchronize()
+    assert fn(buf, n) == 0
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(n, 8).astype(np.int64)
+    t = t[(t[:, 0] != 0) & (t[:, 4] != 0)]  # CTAs that ran an item (idle ones exit early)
+    n = len(t)
+    t0 = t[:, 0].min()
+    names = ["start", "setup", "first_tile", "last_tile", "epilogue", "producer_done"]
+    rel = {nm: (t[:, i] - t0) / 1e3 for i, nm in enumerate(names)}
+    print(json.dumps({"workload": wl["name"], "step": a.step, "ctas": n, "plan": hp.plan["steady"],
+                      "N": hp.st.n_nodes.cpu().tolist()[:8]}))
+    for nm in names:
+        x = rel[nm]
+        print(f"{nm:14s} min {x.min():7.2f} p10 {np.percentile(x, 10):7.2f} p50 {np.median(x):7.2f} "
+              f"p90 {np.percentile(x, 90):7.2f} max {x.max():7.2f} us")
+    dur = {"setup-start": rel["setup"] - rel["start"], "first-setup": rel["first_tile"] - rel["setup"],
+           "tiles": rel["last_tile"] - rel["first_tile"], "epi": rel["epilogue"] - rel["last_tile"],
+           "cta": rel["epilogue"] - rel["start"]}
+    for nm, x in dur.items():
+        print(f"{nm:14s} p10 {np.percentile(x, 10):7.2f} p50 {np.median(x):7.2f} p90 {np.percentile(x, 90):7.2f} us")
+    ntl = t[:, 7]
+    print("tiles per CTA: min", ntl.min(), "median", np.median(ntl), "max", ntl.max(),
+          "| per-tile p50 us", np.median(dur["tiles"] / np.maximum(ntl - 1, 1)))
+    sm = t[:, 6]
+    print("CTAs per SM: max", np.bincount(sm).max(), "SMs used", len(np.unique(sm)))
+    if a.out:
+        np.save(a.out, t)
+
+
+if __name__ == "__main__":
+    main()

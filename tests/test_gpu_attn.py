@@ -130,11 +130,26 @@ def test_rope_kv_append_matches_oracle(dt):
 def test_fused_rope_attention_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W):
     """trie_attn_decode_rope == RoPE at depth (§3.4) + write-before-read append + trie
     attention, vs the oracle (rope_rotate_half + attn_ref on its own trie)."""
+    _fused_case(name, R, b, t_max, Hq, Hkv, D, W)
+
+
+@pytest.mark.parametrize("name,R,b,t_max,Hq,Hkv,D", [
+    ("wide-ragged", 6, 8, 1500, 32, 8, 128),   # Llama shape, requests of 1-24 tiles
+    ("wide-ragged-many", 40, 8, 700, 8, 2, 128),
+    ("wide-ragged-d96", 3, 6, 900, 12, 3, 96),  # Qg = 24, D = 96
+])
+def test_fused_ragged_matches_oracle(name, R, b, t_max, Hq, Hkv, D):
+    """Fused RoPE + wide attention on requests of very different lengths, vs the oracle."""
+    _fused_case(name, R, b, t_max, Hq, Hkv, D, 0, ragged=True)
+
+
+def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False):
     need_gpu()
     from paper_2502_00085_b200.trie import TrieState
     seed = zlib.crc32(name.encode()) % 1000
     V, steps, base = 300, 6, 500000.0
-    prompts, lens = synth.prompts(seed, R, t_max, V)
+    lens = synth.ragged_lens(seed, R, t_max) if ragged else None
+    prompts, lens = synth.prompts(seed, R, t_max, V, lens)
     sels = per_request_selections(seed, R, steps, b, V, 0.5)
     cap = (t_max + b * steps + b + 63) // 64 * 64
     st = TrieState(R, b, t_max, cap, 1, Hq, Hkv, D, V, prompts, lens, window=W, dtype=torch.bfloat16)
