@@ -318,6 +318,169 @@ class HotPath:
         return int(U.sum()) * 2 * Hkv * D * 2 + R * bl * Hq * D * 2 * 2 + int((N - t).clip(min=0).sum()) * 8
 
 
+class BatchPath:
+    """SURVEY §8(f) NEXT-2 baseline: conventional batch beam search (Alg. 1) on
+    the GPU with the same kernels, for the trie-vs-batch comparison on B200.  Every beam
+    owns a private cache holding the whole prompt (replicated b times): a
+    handle of R*b single-beam chains whose fused RoPE + append + attention launch reads each
+    beam's own t+k rows; the top-b is the same trie_beam_step kernel (on a selection-only
+    handle); after it, every beam's cache becomes a copy of its parent beam's (Alg. 1
+    l.6-7; HF _reorder_cache): trie_batch_reorder_kv between two pool sets (ping-pong),
+    copying the generated rows (the identical prompt rows are not copied -- this favours
+    the baseline).  No GC: batch search never frees rows."""
+
+    def __init__(self, wl, dev):
+        import torch
+
+        from paper_2502_00085_b200.trie import TrieState
+        import synth
+        self.torch = torch
+        self.wl = wl
+        L, Hq, Hkv, D, V, t, b, s, R = (wl[k] for k in ("L", "Hq", "Hkv", "D", "V", "t", "b", "s", "R"))
+        self.L, self.Hq, self.Hkv, self.D, self.V, self.t, self.b, self.s, self.R = L, Hq, Hkv, D, V, t, b, s, R
+        self.cap = (t + s + 1 + 63) // 64 * 64
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(1234)
+        lgen = torch.Generator(device=dev)
+        lgen.manual_seed(4321)
+        prompts, lens = synth.prompts(10_000, R, t, V)
+        self.chains = TrieState(R * b, 1, t, self.cap, L, Hq, Hkv, D, V, np.repeat(prompts, b, axis=0),
+                                np.repeat(lens, b), dtype=torch.bfloat16, device=dev)
+        self.sel = TrieState(R, b, t, (t + b * s + b + 63) // 64 * 64, 0, Hq, Hkv, D, V, prompts, lens,
+                             dtype=torch.bfloat16, device=dev)
+        # two pool sets (the reorder is out of place); prompt rows replicated per beam
+        self.P = [self.chains.new_pools() for _ in range(2)]
+        for l in range(L):
+            pk = torch.randn(R, 1, Hkv, t, D, device=dev, generator=gen).to(torch.bfloat16)
+            pv = torch.randn(R, 1, Hkv, t, D, device=dev, generator=gen).to(torch.bfloat16)
+            for kp, vp in self.P:
+                kp[l].view(R, b, Hkv, self.cap, D)[:, :, :, :t] = pk
+                vp[l].view(R, b, Hkv, self.cap, D)[:, :, :, :t] = pv
+        per_layer = R * b * (Hq + 2 * Hkv) * D
+        self.qkv = torch.randn(L * per_layer, device=dev, generator=gen).to(torch.bfloat16)
+        self.views = []
+        for l in range(L):
+            base = l * per_layer
+            q = self.qkv[base: base + R * b * Hq * D].view(R * b, 1, Hq, D)
+            k = self.qkv[base + R * b * Hq * D: base + R * b * (Hq + Hkv) * D].view(R * b, 1, Hkv, D)
+            v = self.qkv[base + R * b * (Hq + Hkv) * D: base + per_layer].view(R * b, 1, Hkv, D)
+            self.views.append((q, k, v))
+        self.out = torch.empty(R * b, 1, Hq, D, dtype=torch.bfloat16, device=dev)
+        self.logits = {"first": torch.randn(R, 1, V, device=dev, generator=lgen) * 3.0,
+                       "steady": torch.randn(R, b, V, device=dev, generator=lgen) * 3.0}
+        self.sel_p = torch.empty(R, b, dtype=torch.int32, device=dev)
+        self.sel_t = torch.empty_like(self.sel_p)
+        self.sel_s = torch.empty(R, b, dtype=torch.float32, device=dev)
+        self.zeros = torch.zeros(R * b, dtype=torch.int32, device=dev)
+        self.graphs = {}
+        self.launches = {}
+        self.k = 0
+
+    def pool_bytes(self):
+        return 2 * 2 * self.L * self.R * self.b * self.Hkv * self.cap * self.D * 2
+
+    def step_ops(self, var, cur):
+        from paper_2502_00085_b200 import _lib
+        ch, se = self.chains, self.sel
+        if var == "first":
+            ch.reset()
+            se.reset()
+        kp, vp = self.P[cur]
+        for l in range(self.L):
+            q, k, v = self.views[l]
+            ch.attn_decode_rope(q, k, v, kp[l], vp[l], self.wl["theta"], self.out, rows_hint=self.t + self.s)
+        se.beam_step(self.logits[var], self.sel_p, self.sel_t, self.sel_s)
+        nk, nv = self.P[1 - cur]
+        _lib.trie_batch_reorder_kv(self.R, self.b, self.Hkv, self.D, self.cap, self.sel_p, ch.prompt_len,
+                                   ch.n_nodes, [kp[l] for l in range(self.L)], [vp[l] for l in range(self.L)],
+                                   [nk[l] for l in range(self.L)], [nv[l] for l in range(self.L)])
+        ch.append(self.zeros, self.sel_t.view(-1))
+
+    def capture(self):
+        from paper_2502_00085_b200 import _lib
+        torch = self.torch
+        for var, cur in (("first", 0), ("steady", 1), ("steady", 0)):
+            g = torch.cuda.CUDAGraph()
+            n0 = _lib.trie_launch_count()
+            with torch.cuda.graph(g):
+                self.step_ops(var, cur)
+            self.graphs[(var, cur)] = g
+            self.launches[(var, cur)] = _lib.trie_launch_count() - n0
+
+    def replay(self):
+        key = ("first" if self.k == 0 else "steady", self.k % 2)
+        self.graphs[key].replay()
+        self.k = (self.k + 1) % self.s
+        return key
+
+
+def run_batch(args):
+    """--impl batch: the NEXT-2 GPU batch-beam-search baseline on the same workload (one GPU;
+    R halved until the two per-beam pool sets fit in 70% of free memory)."""
+    import torch
+
+    from paper_2502_00085_b200 import _lib
+    from paper_2502_00085_b200.build import build
+    build()
+    _lib.load()
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    wl = dict(WORKLOADS[args.workload])
+    if args.beam:
+        wl["b"] = args.beam
+    if args.requests:
+        wl["R"] = args.requests
+    if wl.get("W", 0) or wl.get("kv_shard"):
+        raise SystemExit("--impl batch: dense, unsharded workloads only")
+    free = torch.cuda.mem_get_info()[0]
+    while wl["R"] > 1:
+        cap = (wl["t"] + wl["s"] + 1 + 63) // 64 * 64
+        need = 2 * 2 * wl["L"] * wl["R"] * wl["b"] * wl["Hkv"] * cap * wl["D"] * 2
+        if need <= 0.7 * free:
+            break
+        wl["R"] //= 2
+    bp = BatchPath(wl, dev)
+    for i in range(2):
+        bp.step_ops("first" if i == 0 else "steady", i % 2)
+    torch.cuda.synchronize()
+    bp.capture()
+    bp.k = 0
+    for _ in range(args.warmup):
+        bp.replay()
+    torch.cuda.synchronize()
+    clocks = Clocks(0)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k_hist, launches = [], 0
+    t0.record()
+    for _ in range(args.steps):
+        k_hist.append(bp.k)
+        launches += bp.launches[bp.replay()]
+    t1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    st = bp.chains.status() | bp.sel.status()
+    assert st == 0, f"device status bits {st:#x}"
+    R, b, t, L = bp.R, bp.b, bp.t, bp.L
+    kv_row = L * 2 * bp.Hkv * bp.D * 2
+    k_mean = float(np.mean(k_hist))
+    res = dict(metric="beam-decode steps/s (request-steps/s): GPU batch beam search baseline (NEXT-2)",
+               value=round(R * args.steps / (ms * 1e-3), 2), unit="request-steps/s", n_gpus=1,
+               steps=args.steps, warmup=args.warmup, ms_per_step=round(ms / args.steps, 4),
+               higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16", data="synthetic",
+               impl="batch",
+               config=dict(workload=wl["name"], requests_per_gpu=R, beam=b, prompt_len=t, new_tokens=bp.s,
+                           layers=L, q_heads_per_gpu=bp.Hq, kv_heads_per_gpu=bp.Hkv, head_dim=bp.D,
+                           vocab=bp.V, execution="cuda-graph replay per step",
+                           algorithm="Alg. 1: b private caches per request (prompt replicated), per-beam "
+                                     "attention over t+k rows, same top-b kernel, cache reorder by copy "
+                                     "(generated rows; prompt rows not copied) into a second pool set"),
+               kv_memory=dict(logical_bytes_mean=int(R * b * (t + k_mean) * kv_row),
+                              physical_pool_bytes=int(bp.pool_bytes())),
+               clocks=clk, gpu_launches=int(launches))
+    return res
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -667,7 +830,8 @@ def main():
     ap.add_argument("--requests", type=int, default=0)
     ap.add_argument("--gc-interval", type=int, default=1,
                     help="Alg. 2's GC interval g (1 = every step, the hot path; 0 = never)")
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "batch"],
+                    help="ours | reference (CPU oracle) | batch (GPU batch beam search, NEXT-2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -677,6 +841,9 @@ def main():
         res = run_reference(args)
         if res is not None:
             print(json.dumps(res))
+        return
+    if args.impl == "batch":
+        print(json.dumps(run_batch(args)))
         return
     res, ctx = run_gpu(args)
     if ctx["rank"] == 0:

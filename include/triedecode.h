@@ -169,6 +169,11 @@ int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,
  * appends those leaves' K/V rows (write-before-read, §3.4 / Alg. 3 l.7) before loading
  * the tile.  Other shapes run the two steps as two launches (q, k_new then hold their
  * rotated values).  Arguments as in the two calls; scratch >= trie_attn_scratch_bytes.
+ * Ordering contract: the prompt rows [0, t_r - 1) of the pools (the caller's prefill) must
+ * be written before trie_create / trie_reset and not rewritten while the handle decodes --
+ * the fused kernel may load the tiles below the shortest prompt before its programmatic
+ * dependency wait (prompt nodes never move or change, §3.5 invariant 3; row t_r - 1, the
+ * prompt leaf, is appended by the first call after create / reset).
  */
 int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, const void* v_new,
                           void* k_pool, void* v_pool, float rope_theta, int32_t rows_hint,
@@ -214,6 +219,28 @@ int trie_prune_compact(trie_handle* h, void* const* k_pools_host, void* const* v
  */
 int trie_read_hyps(trie_handle* h, int32_t max_len, int32_t* tokens_host, int32_t* len_host,
                    float* score_host, void* scratch, size_t scratch_bytes, cudaStream_t stream);
+
+/*
+ * Measurement baseline, not part of the trie path: the cache reorder
+ * of conventional batch beam search (Alg. 1; HF _reorder_cache, the paper's
+ * comparison system).  Every beam owns a private cache; after top-b, beam r of request i
+ * continues parent beam j = sel_parent_beam[i*b + r] (Alg. 1 l.6-7), so for every layer l
+ * and KV head h:
+ *   dst_l[i*b + r][h][n] = src_l[i*b + j][h][n]   for prompt_len[i*b + r] <= n < n_rows[i*b + j].
+ * The prompt rows (identical in every beam's cache) are not copied.  Pools per layer:
+ * [R*b][Hkv][capacity][head_dim] elements of elem_bytes (2 = bf16, 4 = fp32); the *_host
+ * arguments are host arrays of n_layers device pointers; src and dst must be distinct.
+ * prompt_len, n_rows: [R*b] int32 (device); sel_parent_beam: [R][b] int32 (device); status:
+ * optional device word, TRIE_ST_PARENT latched for a parent index outside [0, b).
+ * Async on stream; EINVAL for bad shapes or null / in-place pools.
+ */
+int trie_batch_reorder_kv(int32_t n_requests, int32_t beam_width, int32_t n_layers,
+                          int32_t n_kv_heads, int32_t head_dim, int32_t capacity,
+                          int32_t elem_bytes, const int32_t* sel_parent_beam,
+                          const int32_t* prompt_len, const int32_t* n_rows,
+                          void* const* src_k_host, void* const* src_v_host,
+                          void* const* dst_k_host, void* const* dst_v_host, uint32_t* status,
+                          cudaStream_t stream);
 
 /* Read (and keep) the latched device status bits.  Synchronises the stream. */
 int trie_status(trie_handle* h, uint32_t* bits_host, cudaStream_t stream);

@@ -22,7 +22,8 @@ TRIE_ST_CAPACITY, TRIE_ST_PARENT, TRIE_ST_EMPTY_ROW, TRIE_ST_LEAF = 1, 2, 4, 8
 SYMBOLS = ["trie_workspace_bytes", "trie_create", "trie_reset", "trie_destroy", "trie_get_arrays",
            "trie_rope_kv_append", "trie_attn_scratch_bytes", "trie_attn_decode", "trie_beam_step",
            "trie_append", "trie_prune_compact", "trie_read_hyps", "trie_status", "trie_last_error",
-           "trie_version", "trie_launch_count", "trie_attn_decode_rope", "trie_attn_plan_info"]
+           "trie_version", "trie_launch_count", "trie_attn_decode_rope", "trie_attn_plan_info",
+           "trie_batch_reorder_kv"]
 
 
 class trie_cfg(ctypes.Structure):
@@ -71,6 +72,7 @@ def load(path: str = LIB_PATH):
         "trie_last_error": (ctypes.c_char_p, []),
         "trie_version": (ctypes.c_int, []),
         "trie_launch_count": (ctypes.c_ulonglong, []),
+        "trie_batch_reorder_kv": (ctypes.c_int, [I32] * 7 + [P] * 3 + [P] * 4 + [P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -180,6 +182,18 @@ def trie_prune_compact(h, k_pools, v_pools, stream=None):
     vp = (ctypes.c_void_p * max(L, 1))(*[_ptr(x) for x in v_pools])
     _check(load().trie_prune_compact(h, ctypes.cast(kp, ctypes.c_void_p), ctypes.cast(vp, ctypes.c_void_p),
                                      _stream(stream)), "trie_prune_compact")
+
+
+def trie_batch_reorder_kv(R, b, Hkv, D, cap, sel_parent_beam, prompt_len, n_rows, src_k, src_v,
+                          dst_k, dst_v, status=None, stream=None):
+    """NEXT-2 baseline: batch beam search's per-beam cache reorder (see the header).
+    src_*/dst_*: sequences of per-layer [R*b][Hkv][cap][D] pools."""
+    L = len(src_k)
+    arr = [(ctypes.c_void_p * L)(*[_ptr(x) for x in pools]) for pools in (src_k, src_v, dst_k, dst_v)]
+    esz = src_k[0].element_size()
+    _check(load().trie_batch_reorder_kv(R, b, L, Hkv, D, cap, esz, _ptr(sel_parent_beam), _ptr(prompt_len),
+                                        _ptr(n_rows), *arr, _ptr(status), _stream(stream)),
+           "trie_batch_reorder_kv")
 
 
 def trie_read_hyps(h, R: int, b_live: int, max_len: int, scratch, stream=None):

@@ -29,10 +29,11 @@ struct AttnParams {
   const void* v_new;      // [R][b_live][Hkv][D]
   const float2* rope_tab; // [R][b_live][D/2] (cos, sin) of the leaves' depths (per step)
   // pre_tiles > 0: the first pre_tiles 64-slot tiles of every request hold prompt rows
-  // only (host-known minimum prompt length, no window, one split).  Those rows are written
-  // by the caller's prefill before trie_create / trie_reset and never again by any kernel
-  // of the library (the prompt never moves, invariant 3), so their K/V may be loaded
-  // BEFORE griddepcontrol.wait: the first ring stages fill while the predecessor drains.
+  // below t - 1 only (host-known minimum prompt length, no window, one split).  Those rows
+  // are written by the caller's prefill before trie_create / trie_reset and never again by
+  // any kernel of the library (the prompt never moves, invariant 3; row t - 1 is excluded,
+  // the first step appends it as the prompt leaf), so their K/V may be loaded BEFORE
+  // griddepcontrol.wait: the first ring stages fill while the predecessor drains.
   int pre_tiles;
 };
 
