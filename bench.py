@@ -240,7 +240,28 @@ class HotPath:
                         self.launches_per_graph[key] = _lib.trie_launch_count() - n0
                         if timed:
                             self.ev[((var, gc), slot)] = evs
-        # capture ran the host logic of reset/beam_step: leave the host view at "steady"
+        # capture ran the host logic of reset/beam_step: the host view is at "steady" (b
+        # live beams) now, so the roofline's attention-only graph is captured here
+        self._capture_attn_only()
+
+    def _capture_attn_only(self):
+        """Region C's graph: the step's L attention launches (fused a-1 + a-3 where planned)
+        on the steady inputs, with b live beams -- the handle's host view right after the
+        steady step graphs were captured (a later trie_reset sets it back to one beam)."""
+        torch = self.torch
+        st, L = self.st, self.L
+        d = self.inp[("steady", 0)]
+        assert st.b_live == self.b, "attention-only graph must be captured with b live beams"
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for l in range(L):
+                q, k, v = d["views"][l]
+                if self.fused["steady"]:  # idempotent: q is read, the leaves' rows re-written
+                    st.attn_decode_rope(q, k, v, self.kp[l], self.vp[l], self.wl["theta"], d["out"],
+                                        rows_hint=self.rows_hint)
+                else:
+                    st.attn_decode(q, self.kp[l], self.vp[l], d["out"], rows_hint=self.rows_hint)
+        self.attn_graph = g
 
     def gc_now(self, k=None):
         """GC after the append of job step k (0-based) iff Alg. 2's top-of-iteration test
@@ -259,27 +280,15 @@ class HotPath:
         return key
 
     def attn_only_timing(self, reps=10):
-        """Mean duration (us) and algorithmic bytes of one trie_attn_decode launch: a graph
-        of the L layers' launches on the steady inputs, replayed `reps` times."""
+        """Mean duration (us) and algorithmic bytes of one trie_attn_decode launch: the
+        graph of the L layers' steady launches (captured with the step graphs), replayed
+        `reps` times on the trie the timed steps left."""
         torch = self.torch
-        st, L = self.st, self.L
-        d = self.inp[("steady", 0)]
+        L = self.L
         if self.k == 0:  # a job boundary: the trie holds only the prompt; step once
             self.replay(0)
         torch.cuda.synchronize()
-
-        def launches():  # the launch the step makes (fused a-1 + a-3 where planned)
-            for l in range(L):
-                q, k, v = d["views"][l]
-                if self.fused["steady"]:  # idempotent: q is read, the leaves' rows re-written
-                    st.attn_decode_rope(q, k, v, self.kp[l], self.vp[l], self.wl["theta"], d["out"],
-                                        rows_hint=self.rows_hint)
-                else:
-                    st.attn_decode(q, self.kp[l], self.vp[l], d["out"], rows_hint=self.rows_hint)
-        launches()  # warm (scratch sizing)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            launches()
+        g = self.attn_graph
         g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -423,13 +423,16 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.aux = scratch;
   p.part = (float*)((char*)scratch + pl.counter_bytes);
   p.splits = pl.splits;
-  if (cfg->window == 0 && pl.splits == 1 && prefetch_enabled()) {
+  if (cfg->window == 0 && prefetch_enabled()) {
     // tiles below the shortest prompt's last row hold prompt rows that no kernel of the
     // library writes (AttnParams::pre_tiles); row t - 1 is excluded: it is the first
-    // step's leaf, appended by the b_live = 1 call
+    // step's leaf, appended by the b_live = 1 call.  Only split 0 prefetches; its range
+    // ceil(tiles / splits) >= ceil((pre + 1) / splits) tiles bounds the count.
     int t_min = INT32_MAX;
     for (int32_t t : h->host_tlen) t_min = t < t_min ? t : t_min;
-    p.pre_tiles = (t_min - 1) / 64;
+    const int pre = (t_min - 1) / 64;
+    const int per_min = (pre + 1 + pl.splits - 1) / pl.splits;
+    p.pre_tiles = pre < per_min ? pre : per_min;
   }
   return trie::launch_attn_tc(p, stream);
 }

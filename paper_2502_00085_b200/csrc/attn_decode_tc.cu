@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // prompt-only tiles loaded before the wait (see AttnParams::pre_tiles)
-  const int npre = min(p.pre_tiles, C::STAGES);
+  const int npre = split == 0 ? min(p.pre_tiles, C::STAGES) : 0;
   if (threadIdx.x == 0 && npre > 0)
     prefetch_prompt_tiles<D, C::STAGES>(&kmap, &vmap, p, r, h, ring, full, npre);
   pdl_wait();  // the shared-memory setup above ran before the predecessor finished
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // prompt-only tiles loaded before the wait (see AttnParams::pre_tiles)
-  const int npre = min(p.pre_tiles, C::STAGES);
+  const int npre = split == 0 ? min(p.pre_tiles, C::STAGES) : 0;
   if (threadIdx.x == 0 && npre > 0)
     prefetch_prompt_tiles<D, C::STAGES>(&kmap, &vmap, p, r, h, ring, full, npre);
   pdl_wait();  // the shared-memory setup above ran before the predecessor finished
@@ -872,10 +872,10 @@ static const TcKernel* select_tc(int D, int Qg, bool rope = false) {
   return nullptr;
 }
 
-// The fused RoPE + append variants: narrow (Qg <= 16) and wide at Qg <= 32.
+// The fused RoPE + append variants: narrow (Qg <= 16), wide at Qg <= 32, tcgen05.
 bool attn_rope_fusable(const AttnParams& p) {
   const int Qg = p.b_live * (p.Hq / p.Hkv);
-  return attn_tc_supported(p) && !attn_umma_eligible(p) && Qg <= 32;
+  return attn_tc_supported(p) && (attn_umma_eligible(p) || Qg <= 32);
 }
 
 bool attn_tc_shape_ok(const AttnParams& p) {
@@ -902,9 +902,15 @@ int attn_plan_splits(const AttnParams& p, int rows_est, int sms) {
     if (k) occ = k->occ;
   }
   const int slots = occ * sms;
+  const int max_by_rows = rows_est / 128 > 0 ? rows_est / 128 : 1;
+  static int forced = -1;  // TRIE_ATTN_SPLITS=n: experiments only
+  if (forced < 0) {
+    const char* e = getenv("TRIE_ATTN_SPLITS");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced > 0) return std::min(std::min(forced, max_by_rows), 64);
   if (units >= slots) return 1;
   int splits = slots / units;
-  const int max_by_rows = rows_est / 128 > 0 ? rows_est / 128 : 1;
   if (splits > max_by_rows) splits = max_by_rows;
   if (splits > 64) splits = 64;
   return splits < 1 ? 1 : splits;

@@ -139,7 +139,7 @@ struct UCfg {
   static constexpr int OFF_X = OFF_Q + QBYTES;           // epilogue (m, l) exchange [2][4][32] f32x2
   static constexpr int OFF_BAR = OFF_X + 2 * 4 * 32 * 8;
   static constexpr int NSB = 4;                    // S buffers
-  static constexpr int NBAR = 2 * STK + 2 * STV + 3 * NSB;  // K/V full/empty, s_full, p_full, pv_done
+  static constexpr int NBAR = 2 * STK + 2 * STV + 3 * NSB + 1;  // K/V full/empty, s_full, p_full, pv_done, app_done
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 64 + 1024;
   static constexpr int NSW = 8;                // softmax warps (2 groups x 4 sub-partitions)
   static constexpr int THREADS = (4 + NSW) * 32; // + K producer, PV, QK, V producer (last)
@@ -153,7 +153,11 @@ struct UCfg {
 #define TRIE_UMMA_TRACE 0
 #endif
 
-template <int D, int STK, int STV>
+// ROPE: fused a-1 (trie_attn_decode_rope), as in the narrow / wide kernels -- the softmax
+// warps stage Q rotated at the beams' depths (rotate-half partners are the chunks at col
+// and col + D/2) and, in the same pass, rotate and append the leaves' K/V rows of this
+// CTA's tiles; both producers wait for that append before the first leaf tile.
+template <int D, int STK, int STV, bool ROPE = false>
 __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p) {
@@ -169,7 +173,8 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
   uint64_t* s_full = emptyV + STV;
   uint64_t* p_full = s_full + C::NSB;
   uint64_t* pv_done = p_full + C::NSB;
-  uint32_t* tmem_slot = (uint32_t*)(pv_done + C::NSB);
+  uint64_t* app_done = pv_done + C::NSB;
+  uint32_t* tmem_slot = (uint32_t*)(app_done + 1);
   ItemInfo* info = (ItemInfo*)(tmem_slot + 4);
 
   const int h = blockIdx.x, r = blockIdx.y, split = blockIdx.z;
@@ -193,6 +198,7 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
       mbar_init(&p_full[e], n_live);  // the live softmax warps of the tile's group
       mbar_init(&pv_done[e], 1);
     }
+    mbar_init(app_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   pdl_wait();  // the shared-memory setup above ran before the predecessor finished
@@ -222,8 +228,10 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
 
   if (warp == 0 || warp == 3 + C::NSW) {
     // ============ TMA producers: warp 0 = K tiles, the last warp = V tiles + mask words ============
+    const int first_leaf = ROPE ? it.N - p.b_live : INT_MAX;
     if (lane == 0) {
       const bool isv = warp != 0;
+      bool appended = !ROPE;
       const int row_base = (r * p.Hkv + h) * p.cap;
       const size_t mbase = (size_t)r * p.cap;
       const int ns = isv ? STV : STK;
@@ -235,6 +243,10 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
         const int s = i % ns;
         mbar_wait(&eb[s], ((uint32_t)(i / ns) & 1u) ^ 1u);
         TRC(i, isv ? 12 : 7);
+        if (!appended && (it.tile0 + i + 1) * TC_TR > first_leaf) {
+          mbar_wait(app_done, 0u);  // leaf rows written (and fenced) by warp 0's lanes 1..31
+          appended = true;
+        }
         const int n0 = (it.tile0 + i) * TC_TR;
         // mask / depth words clamped to the [R][cap] arrays (cap % 4 == 0: 16-byte granules)
         const uint32_t mdb = isv ? (uint32_t)min(TC_TR, p.cap - n0) * 4u : 0u;
@@ -320,7 +332,38 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
       const __nv_bfloat16* q = (const __nv_bfloat16*)p.q;
       const int chunks = 128 * (D / 8);
       const float inv_g = 1.f / (float)g;  // exact: m < 128, g <= 128
-      for (int c = tid; c < chunks; c += C::NSW * 32) {
+      if constexpr (ROPE) {  // chunk pairs (col, col + D/2), rotated like trie_rope_kv_append
+        constexpr int HALF = D / 2;
+        for (int c = tid; c < 128 * (HALF / 8); c += C::NSW * 32) {
+          const int m = c / (HALF / 8), col = (c % (HALF / 8)) * 8;
+          int4 y1 = make_int4(0, 0, 0, 0), y2 = make_int4(0, 0, 0, 0);
+          if (m < Qg) {
+            const int j = __float2int_rz(((float)m + 0.5f) * inv_g);
+            const __nv_bfloat16* src = q + (((size_t)r * p.b_live + j) * p.Hq + h * g + m - j * g) * D;
+            const int4 a = *(const int4*)(src + col), b2 = *(const int4*)(src + HALF + col);
+            const float4* tb = (const float4*)(p.rope_tab + ((size_t)r * p.b_live + j) * HALF + col);
+            const __nv_bfloat162* a2 = (const __nv_bfloat162*)&a;
+            const __nv_bfloat162* bb = (const __nv_bfloat162*)&b2;
+            __nv_bfloat162* o1 = (__nv_bfloat162*)&y1;
+            __nv_bfloat162* o2 = (__nv_bfloat162*)&y2;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float4 tt = __ldg(tb + u);
+              const float2 x1 = __bfloat1622float2(a2[u]), x2 = __bfloat1622float2(bb[u]);
+              o1[u] = __floats2bfloat162_rn(x1.x * tt.x - x2.x * tt.y, x1.y * tt.z - x2.y * tt.w);
+              o2[u] = __floats2bfloat162_rn(x2.x * tt.x + x1.x * tt.y, x2.y * tt.z + x1.y * tt.w);
+            }
+          }
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int cc = col + hh * HALF;
+            const int box = cc / TC_CW;
+            const uint32_t o = (uint32_t)m * 64u + (uint32_t)(cc % TC_CW) * 2u;
+            *(int4*)(qsm + box * 128 * 64 + (o ^ (((o >> 7) & 3u) << 4))) = hh ? y2 : y1;
+          }
+        }
+      }
+      for (int c = ROPE ? chunks : tid; c < chunks; c += C::NSW * 32) {
         const int m = c / (D / 8), col = (c % (D / 8)) * 8;
         int4 v = make_int4(0, 0, 0, 0);
         if (m < Qg) {
@@ -331,8 +374,12 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
         const uint32_t o = (uint32_t)m * 64u + (uint32_t)(col % TC_CW) * 2u;
         *(int4*)(qsm + box * 128 * 64 + (o ^ (((o >> 7) & 3u) << 4))) = v;
       }
+      if constexpr (ROPE)  // the leaves' K/V rows of this CTA's tiles (fused a-1), then fenced
+        append_leaves_rope_work<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + ntiles) * TC_TR, tid,
+                                   C::NSW * 32, it.N - p.b_live);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"r"(QBAR_THREADS));
+      if (ROPE && tid == 0) mbar_arrive(app_done);  // every softmax thread's append is fenced
     }
     if (sp < n_live) {  // warps of padding-only sub-partitions have nothing to do
       const bool qvalid = row < Qg;
@@ -547,11 +594,11 @@ struct UKernel {
   const void* fn;
   int smem, threads, occ;
 };
-template <int D, int STK, int STV>
+template <int D, int STK, int STV, bool ROPE = false>
 static const UKernel& uk() {
   static const UKernel k = [] {
     using C = UCfg<D, STK, STV>;
-    auto kern = k_attn_umma<D, STK, STV>;
+    auto kern = k_attn_umma<D, STK, STV, ROPE>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     int occ = 0;
@@ -562,7 +609,8 @@ static const UKernel& uk() {
 }
 
 template <int D>
-static const UKernel& select_ud() {
+static const UKernel& select_ud(bool rope) {
+  if (rope) return uk<D, 4, 6, true>();  // fused a-1: the default stage split only
   // TRIE_UMMA_ST: V ring stages (4, 6 = default, 8; the K ring has 4, 3 with 8 V stages)
   static int st = -1;
   if (st < 0) {
@@ -573,11 +621,11 @@ static const UKernel& select_ud() {
   if (st >= 6) return uk<D, 4, 6>();
   return uk<D, 4, 4>();
 }
-static const UKernel* select_u(int D) {
+static const UKernel* select_u(int D, bool rope = false) {
   switch (D) {
-    case 64: return &select_ud<64>();
-    case 96: return &select_ud<96>();
-    case 128: return &select_ud<128>();
+    case 64: return &select_ud<64>(rope);
+    case 96: return &select_ud<96>(rope);
+    case 128: return &select_ud<128>(rope);
   }
   return nullptr;
 }
@@ -610,7 +658,7 @@ int attn_umma_occ(const AttnParams& p) {
 }
 
 int launch_attn_umma(const AttnParams& p, cudaStream_t s) {
-  const UKernel* k = select_u(p.D);
+  const UKernel* k = select_u(p.D, p.rope != 0);
   if (!k) return trie_set_error(TRIE_EINVAL, "tcgen05 attention: unsupported head_dim %d", p.D);
   CUtensorMap km, vm;
   const long rows = (long)p.R * p.Hkv * p.cap;

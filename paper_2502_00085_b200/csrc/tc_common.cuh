@@ -171,10 +171,12 @@ __device__ __forceinline__ void item_setup(const AttnParams& p, int r, int split
 // (async proxy) reads of lane 0, which waits on app_done before the tile of the first leaf.
 // The leaves are the last b_live slots (invariant 2 of the handle's trie: appends go to
 // the end, compaction is stable), so leaf j's slot is first_leaf + j -- no load of leaf[].
+// The append itself, by `nw` workers (worker index w): 16-byte chunks of the leaves' K (rotated)
+// and V rows in [slot_lo, slot_hi).  The caller fences and signals (see below).
 template <int D>
-__device__ __forceinline__ void append_leaves_rope(const AttnParams& p, int r, int h, int slot_lo,
-                                                   int slot_hi, int lane, uint64_t* app_done,
-                                                   int first_leaf) {
+__device__ __forceinline__ void append_leaves_rope_work(const AttnParams& p, int r, int h,
+                                                        int slot_lo, int slot_hi, int w, int nw,
+                                                        int first_leaf) {
   constexpr int HALF = D / 2, CH = HALF / 8;
   static_assert(HALF % 8 == 0, "head_dim must be a multiple of 16");
   const __nv_bfloat16* __restrict__ kn = (const __nv_bfloat16*)p.k_new;
@@ -182,7 +184,7 @@ __device__ __forceinline__ void append_leaves_rope(const AttnParams& p, int r, i
   __nv_bfloat16* kpool = (__nv_bfloat16*)p.k;
   __nv_bfloat16* vpool = (__nv_bfloat16*)p.v;
   const int nk = p.b_live * CH, nv = p.b_live * (D / 8);
-  for (int e = lane - 1; e < nk + nv; e += 31) {
+  for (int e = w; e < nk + nv; e += nw) {
     const int j = e < nk ? e / CH : (e - nk) / (D / 8);
     const int slot = first_leaf + j;
     if (slot < slot_lo || slot >= slot_hi) continue;
@@ -214,7 +216,16 @@ __device__ __forceinline__ void append_leaves_rope(const AttnParams& p, int r, i
       *(int4*)(dst + d) = __ldg((const int4*)(vn + (rj * p.Hkv + h) * D + d));
     }
   }
+  // the generic-proxy writes must be visible to the TMA (async proxy) reads of the tile
   asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Lanes 1..31 of the producer warp append, then lane 1 arrives on app_done.
+template <int D>
+__device__ __forceinline__ void append_leaves_rope(const AttnParams& p, int r, int h, int slot_lo,
+                                                   int slot_hi, int lane, uint64_t* app_done,
+                                                   int first_leaf) {
+  append_leaves_rope_work<D>(p, r, h, slot_lo, slot_hi, lane - 1, 31, first_leaf);
   __syncwarp(0xfffffffeu);
   if (lane == 1) mbar_arrive(app_done);
 }

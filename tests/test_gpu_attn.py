@@ -125,7 +125,10 @@ def test_rope_kv_append_matches_oracle(dt):
     ("wide-fused", 1, 8, 130, 8, 2, 128, 0),      # Qg = 32: wide kernel, fused
     ("wide-fused-llama", 2, 8, 150, 32, 8, 128, 0),
     ("wide-fused-split", 1, 6, 1000, 16, 4, 64, 0),  # Qg = 24, D = 64, split K
-    ("umma-unfused", 1, 16, 130, 8, 2, 128, 0),   # Qg = 64: tcgen05, two-launch fallback
+    ("umma-fused", 1, 16, 130, 8, 2, 128, 0),     # Qg = 64: tcgen05, fused
+    ("umma-fused-swa", 2, 16, 400, 8, 2, 128, 100),
+    ("umma-fused-d96", 1, 12, 300, 8, 2, 96, 0),  # Qg = 48
+    ("umma-fused-d64-split", 1, 32, 1500, 4, 2, 64, 0),  # Qg = 64, split K: leaves in the last split
 ])
 def test_fused_rope_attention_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W):
     """trie_attn_decode_rope == RoPE at depth (§3.4) + write-before-read append + trie
