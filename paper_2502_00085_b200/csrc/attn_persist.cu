@@ -16,6 +16,7 @@
 //    merges all partials -- the split combine is fused, no second launch.
 //  * Counters live at the start of the caller's scratch; they must be zero before the
 //    first launch and every launch returns them to zero.
+#include <algorithm>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -714,6 +715,8 @@ int attn_persist_splits(const AttnParams& p, int rows_est, int sms) {
   const int occ = k ? k->occ : 2;
   const int items = p.R * p.Hkv;
   const int tiles = (rows_est + TC_TR - 1) / TC_TR;
+  const char* fe = getenv("TRIE_ATTN_SPLITS");  // experiments only
+  if (fe && atoi(fe) > 0) return std::min(atoi(fe), 64);
   const long target = 3L * occ * sms;
   int ct = (int)(((long)items * tiles + target - 1) / target);
   if (ct < 2) ct = 2;

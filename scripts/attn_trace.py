@@ -77,6 +77,14 @@ def main():
           "| per-tile p50 us", np.median(dur["tiles"] / np.maximum(ntl - 1, 1)))
     sm = t[:, 6]
     print("CTAs per SM: max", np.bincount(sm).max(), "SMs used", len(np.unique(sm)))
+    # occupancy over time: CTAs resident (start..epilogue) and streaming (first..last tile)
+    end = rel["epilogue"].max()
+    bins = np.linspace(0, end, 21)
+    res = [int(((rel["start"] <= b) & (rel["epilogue"] > b)).sum()) for b in bins[:-1]]
+    stream = [int(((rel["first_tile"] <= b) & (rel["last_tile"] > b)).sum()) for b in bins[:-1]]
+    print("t(us)    ", " ".join(f"{b:5.0f}" for b in bins[:-1]))
+    print("resident ", " ".join(f"{x:5d}" for x in res))
+    print("streaming", " ".join(f"{x:5d}" for x in stream))
     if a.out:
         np.save(a.out, t)
 
