@@ -78,10 +78,11 @@ def main():
     tag, wl, lcsv, attn = argv[:4]
     aux = argv[4] if len(argv) > 4 else None
     os.makedirs(PROF, exist_ok=True)
-    table, _ = launches(lcsv)
-    with open(os.path.join(PROF, f"{tag}_{wl}_launches.md"), "w") as f:
-        f.write(f"# {tag} {wl}: launch list (ncu --metrics gpu__time_duration.sum --clock-control none)\n\n")
-        f.write("Cold-cache, serialised per-launch times (compare shares, not absolutes).\n\n" + table + "\n")
+    table = launches(lcsv)[0] if lcsv != "-" else None
+    if table is not None:
+        with open(os.path.join(PROF, f"{tag}_{wl}_launches.md"), "w") as f:
+            f.write(f"# {tag} {wl}: launch list (ncu --metrics gpu__time_duration.sum --clock-control none)\n\n")
+            f.write("Cold-cache, serialised per-launch times (compare shares, not absolutes).\n\n" + table + "\n")
     lines = [f"# {tag} {wl}: ncu --set full captures\n"]
     dram = []
     for rep in [attn] + ([aux] if aux else []):
