@@ -146,14 +146,14 @@ def test_fused_ragged_matches_oracle(name, R, b, t_max, Hq, Hkv, D):
     _fused_case(name, R, b, t_max, Hq, Hkv, D, 0, ragged=True)
 
 
-def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False):
+def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False, steps=6, rho=0.5):
     need_gpu()
     from paper_2502_00085_b200.trie import TrieState
     seed = zlib.crc32(name.encode()) % 1000
-    V, steps, base = 300, 6, 500000.0
+    V, base = 300, 500000.0
     lens = synth.ragged_lens(seed, R, t_max) if ragged else None
     prompts, lens = synth.prompts(seed, R, t_max, V, lens)
-    sels = per_request_selections(seed, R, steps, b, V, 0.5)
+    sels = per_request_selections(seed, R, steps, b, V, rho)
     cap = (t_max + b * steps + b + 63) // 64 * 64
     st = TrieState(R, b, t_max, cap, 1, Hq, Hkv, D, V, prompts, lens, window=W, dtype=torch.bfloat16)
     kp, vp = st.new_pools()
@@ -214,3 +214,29 @@ def test_attention_plan_paths():
     assert path(4, 32, 8, 128, 8448, 8320).startswith("tcgen05")       # sweep, Qg = 16
     assert path(16, 32, 8, 128, 448, 406).startswith("tcgen05")        # Qg = 64
     assert path(2, 32, 8, 128, 8448, 8320).startswith("narrow")        # Qg = 8
+
+
+def _fuzz_cases(n=24, seed=2502):
+    """Seeded random shapes for the fused path (the call bench.py times): ragged prompts
+    from 1 row to several tiles (pre-wait prefetch from 0 to many tiles, prompts that end on
+    and off tile boundaries), b in 1..16, GQA groups 1..8, D in {64, 96, 128}, windows
+    shorter and longer than the tries, narrow / wide / tcgen05 kernels."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        D = int(rng.choice([64, 96, 128]))
+        Hkv = int(rng.choice([1, 2, 4]))
+        g = int(rng.choice([1, 2, 4, 8]))
+        b = int(rng.choice([1, 2, 3, 4, 5, 8, 12, 16]))
+        t_max = int(rng.choice([1, 17, 64, 65, 128, 150, 300, 513]))
+        W = int(rng.choice([0, 0, 1, 7, 64, 200]))
+        out.append((f"fuzz{i}", int(rng.integers(1, 5)), b, t_max, g * Hkv, Hkv, D, W,
+                    bool(rng.integers(0, 2)), int(rng.integers(1, 9)), float(rng.choice([0.0, 0.5, 1.0]))))
+    return out
+
+
+@pytest.mark.parametrize("name,R,b,t_max,Hq,Hkv,D,W,ragged,steps,rho", _fuzz_cases(),
+                         ids=[c[0] for c in _fuzz_cases()])
+def test_fused_fuzz_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W, ragged, steps, rho):
+    """trie_attn_decode_rope on seeded random shapes vs the oracle (bf16, 2e-2)."""
+    _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=ragged, steps=steps, rho=rho)
