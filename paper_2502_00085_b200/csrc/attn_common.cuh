@@ -35,6 +35,7 @@ struct AttnParams {
   // the first step appends it as the prompt leaf), so their K/V may be loaded BEFORE
   // griddepcontrol.wait: the first ring stages fill while the predecessor drains.
   int pre_tiles;
+  int half_tiles;         // narrow / wide: the last tile of an item loads 32-row boxes when <= 32 rows remain
 };
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);

@@ -70,7 +70,9 @@ struct NarrowCfg {
 template <int D, int NQ, int ST, bool ROPE = false>
 __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUtensorMap kmap,
                                                     const __grid_constant__ CUtensorMap vmap,
-                                                    const AttnParams p) {
+                                                    const AttnParams p,
+                                                    const __grid_constant__ CUtensorMap kmh,
+                                                    const __grid_constant__ CUtensorMap vmh) {
   using C = NarrowCfg<D, NQ, ST, ROPE>;
   using RG = typename C::RG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -124,14 +126,14 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       while (fill > npre && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr,
-                                    INT_MAX, npre, fill);
+                                    INT_MAX, npre, fill, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
       __syncwarp();
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
-                                    first_leaf, max(fill, npre));
+                                    first_leaf, max(fill, npre), INT_MAX, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
     } else if (lane == 0) {
       producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr, INT_MAX,
-                                  npre);
+                                  npre, INT_MAX, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
     }
     if constexpr (ROPE) if (lane != 0)
       append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane, app_done,
@@ -416,7 +418,8 @@ struct WideCfg {
 template <int D, int MT, int RS, bool ROPE = false>
 __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
-    const AttnParams p) {
+    const AttnParams p, const __grid_constant__ CUtensorMap kmh,
+    const __grid_constant__ CUtensorMap vmh) {
   using C = WideCfg<D, MT, RS>;
   using RG = typename C::RG;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -467,17 +470,17 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       while (fill > npre && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr,
-                                    INT_MAX, npre, fill);
+                                    INT_MAX, npre, fill, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
       __syncwarp();
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
-                                    first_leaf, max(fill, npre));
+                                    first_leaf, max(fill, npre), INT_MAX, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
       else
         append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane,
                               app_done, first_leaf);
     } else if (lane == 0) {
       producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr, INT_MAX,
-                                  npre);
+                                  npre, INT_MAX, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
     }
     ATTN_TRC(lane == 0, 5);
     return;
@@ -746,12 +749,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const void* base, int D, long rows) {
+static int make_map(CUtensorMap* map, const void* base, int D, long rows, int box_rows) {
   auto enc = get_encode();
   if (!enc) return trie_set_error(TRIE_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-  cuuint32_t box[2] = {(cuuint32_t)TC_CW, (cuuint32_t)TC_TR};
+  cuuint32_t box[2] = {(cuuint32_t)TC_CW, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult rc = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -766,15 +769,15 @@ static int make_map(CUtensorMap* map, const void* base, int D, long rows) {
 struct MapEntry {
   const void* base;
   long rows;
-  int D;
+  int D, box_rows;
   CUtensorMap map;
 };
-int cached_tensor_map(CUtensorMap* out, const void* base, int D, long rows) {
-  static MapEntry cache[512];
-  const size_t slot = (((uintptr_t)base >> 8) ^ ((uintptr_t)base >> 20)) % 512;
+int cached_tensor_map(CUtensorMap* out, const void* base, int D, long rows, int box_rows) {
+  static MapEntry cache[1024];
+  const size_t slot = ((((uintptr_t)base >> 8) ^ ((uintptr_t)base >> 20)) * 2 + (box_rows != TC_TR)) % 1024;
   MapEntry& e = cache[slot];
-  if (e.base != base || e.rows != rows || e.D != D) {
-    const int rc = make_map(&e.map, base, D, rows);
+  if (e.base != base || e.rows != rows || e.D != D || e.box_rows != box_rows) {
+    const int rc = make_map(&e.map, base, D, rows, box_rows);
     if (rc) {
       e.base = nullptr;
       return rc;
@@ -782,6 +785,7 @@ int cached_tensor_map(CUtensorMap* out, const void* base, int D, long rows) {
     e.base = base;
     e.rows = rows;
     e.D = D;
+    e.box_rows = box_rows;
   }
   *out = e.map;
   return TRIE_OK;
@@ -920,13 +924,21 @@ int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
   if (attn_umma_eligible(p)) return launch_attn_umma(p, s);
   const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv), p.rope != 0);
   if (!k) return trie_set_error(TRIE_EINVAL, "tensor-core attention: unsupported head_dim %d", p.D);
-  CUtensorMap km, vm;
+  CUtensorMap km, vm, kmh, vmh;
   const long rows = (long)p.R * p.Hkv * p.cap;
   int rc = cached_tensor_map(&km, p.k, p.D, rows);
   if (!rc) rc = cached_tensor_map(&vm, p.v, p.D, rows);
+  if (!rc) rc = cached_tensor_map(&kmh, p.k, p.D, rows, TC_TR / 2);
+  if (!rc) rc = cached_tensor_map(&vmh, p.v, p.D, rows, TC_TR / 2);
   if (rc) return rc;
   AttnParams pp = p;
-  void* args[3] = {(void*)&km, (void*)&vm, (void*)&pp};
+  static int half = -1;  // TRIE_HALF_TILE=0 disables the 32-row last tiles (A/B experiments)
+  if (half < 0) {
+    const char* e = getenv("TRIE_HALF_TILE");
+    half = (e && e[0] == '0') ? 0 : 1;
+  }
+  pp.half_tiles = half;
+  void* args[5] = {(void*)&km, (void*)&vm, (void*)&pp, (void*)&kmh, (void*)&vmh};
   launch_k_ptr(k->fn, dim3(p.Hkv, p.R, p.splits), dim3(k->threads), (size_t)k->smem, s, args);
   rc = trie_check_launch("k_attn_tc");
   if (rc) return rc;

@@ -644,7 +644,6 @@ __global__ void __launch_bounds__(PCfg<D, QMAX, ST, NCW>::THREADS) k_attn_persis
 }
 
 // ---- host side ---------------------------------------------------------------------------
-int cached_tensor_map(CUtensorMap* out, const void* base, int D, long rows);  // attn_decode_tc.cu
 
 struct PKernel {
   const void* fn;

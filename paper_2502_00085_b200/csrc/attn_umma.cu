@@ -588,7 +588,6 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
 }
 
 // ---- host side ---------------------------------------------------------------------------
-int cached_tensor_map(CUtensorMap* out, const void* base, int D, long rows);
 
 struct UKernel {
   const void* fn;

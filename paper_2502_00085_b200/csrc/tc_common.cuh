@@ -13,6 +13,10 @@
 namespace trie {
 
 constexpr int TC_TR = 64;  // slots per tile
+
+// TMA maps of a layer's pool ([rows][D] bf16, 64-byte swizzle, 32-column boxes of box_rows
+// rows), encoded once per (base, rows, D, box rows) -- attn_decode_tc.cu
+int cached_tensor_map(CUtensorMap* out, const void* base, int D, long rows, int box_rows = TC_TR);
 constexpr int TC_CW = 32;  // elements per swizzle box column (64 bytes, SWIZZLE_64B)
 
 // ---- PTX helpers -------------------------------------------------------------------------
@@ -258,7 +262,13 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
                                               const ItemInfo& it, uint8_t* ring, uint64_t* full,
                                               uint64_t* empty, uint64_t* app_done = nullptr,
                                               int first_leaf_slot = INT_MAX, int i_begin = 0,
-                                              int i_end = INT_MAX, uint32_t* trc = nullptr) {
+                                              int i_end = INT_MAX, uint32_t* trc = nullptr,
+                                              const CUtensorMap* kmh = nullptr,
+                                              const CUtensorMap* vmh = nullptr) {
+  // kmh / vmh: maps with 32-row boxes.  The request's last tile, when it holds <= 32 rows
+  // below N, loads only its first 32 rows (the rest of the stage keeps the finite K/V of
+  // an earlier tile -- hence only stages already used, i >= STAGES -- and those rows are
+  // masked, n >= N): the 64-row tile granularity over-fetched ~half a tile per item.
   using RG = Ring<D, STAGES>;
   const int row_base = (r * p.Hkv + h) * p.cap;
   const size_t mbase = (size_t)r * p.cap;
@@ -278,11 +288,14 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
     const int n0 = (it.tile0 + i) * TC_TR;
     // mask / depth words clamped to the [R][cap] arrays (cap % 4 == 0: 16-byte granules)
     const uint32_t mdb = (uint32_t)min(TC_TR, p.cap - n0) * 4u;
-    mbar_expect_tx(&full[s], 2 * RG::TILE_BYTES + 2 * mdb);
+    const bool half = kmh != nullptr && i >= STAGES && it.N - n0 <= TC_TR / 2;
+    mbar_expect_tx(&full[s], (half ? RG::TILE_BYTES : 2 * RG::TILE_BYTES) + 2 * mdb);
+    const CUtensorMap* km = half ? kmh : kmap;
+    const CUtensorMap* vm = half ? vmh : vmap;
 #pragma unroll
     for (int bx = 0; bx < D / TC_CW; ++bx) {
-      tma_load_2d(st + bx * TC_TR * 64, kmap, bx * TC_CW, row_base + n0, &full[s]);
-      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vmap, bx * TC_CW, row_base + n0, &full[s]);
+      tma_load_2d(st + bx * TC_TR * 64, km, bx * TC_CW, row_base + n0, &full[s]);
+      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vm, bx * TC_CW, row_base + n0, &full[s]);
     }
     bulk_load_1d(st + 2 * RG::TILE_BYTES, p.mask + mbase + n0, mdb, &full[s]);
     bulk_load_1d(st + 2 * RG::TILE_BYTES + TC_TR * 4, p.depth + mbase + n0, mdb, &full[s]);
