@@ -129,3 +129,19 @@ def test_bench_batch_arm_runs():
     assert out.returncode == 0, out.stderr[-2000:]
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["impl"] == "batch" and res["value"] > 0 and res["gpu_launches"] > 0
+
+
+def test_bench_two_ranks_request_dp():
+    """bench.py's N > 1 path (request data parallel, one process per rank, max-over-ranks
+    timing) on one GPU: two ranks share cuda:0 through the gloo test mode."""
+    need_gpu()
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--workload", "llama", "--requests", "4", "--steps", "6", "--warmup", "3",
+                          "--no-cpu-baseline", "--no-e2e"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = json.loads([l for l in out.stdout.strip().splitlines() if l.startswith("{")][-1])
+    assert res["n_gpus"] == 2 and res["value"] > 0 and res["scaling"] == "weak"
+    assert res["config"]["parallelism"] == "request-dp2"
