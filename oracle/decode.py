@@ -10,7 +10,8 @@ Both beam decoders call the same one-token `model.forward(token, pos, ctx)` and 
 With identical per-query row lists the two are bitwise equal in float64 -- the paper's
 "theoretically equivalent" claim made checkable.
 
-Fixed new-token count s (reading R5: no EOS on the hot path), L = t + s (reading R20).
+Fixed new-token count s (reading R5: no EOS on the hot path), L = t + s (reading R20);
+optionally EOS as an absorbing token (`eos`, reading R5b, select.absorb_eos).
 TEST INFRASTRUCTURE ONLY.
 """
 from __future__ import annotations
@@ -19,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .select import select_topb
+from .select import absorb_eos, select_topb
 from .trie import Trie, build_mask, garbage_collect, update_mask, window_allow
 
 
@@ -54,13 +55,15 @@ def _forward_beam(model, beam: _Beam, window: int):
     return lp
 
 
-def batch_beam_search(model, prompt, b: int, s: int, window: int = 0) -> DecodeResult:
+def batch_beam_search(model, prompt, b: int, s: int, window: int = 0, eos=None) -> DecodeResult:
     L_layers = model.cfg.L
     beams = [_Beam(prompt, [[] for _ in range(L_layers)], 0.0)]      # l.1-2
     res = DecodeResult(hyps=[], best=None)
     t = len(prompt)
     for i in range(t, t + s):                                          # l.3
         lp_rows = [_forward_beam(model, bm, window) for bm in beams]   # l.4-5
+        fin = [len(bm.tokens) > t and bm.tokens[-1] == eos for bm in beams]
+        lp_rows = absorb_eos(lp_rows, fin, eos)                        # reading R5b
         sel = select_topb([bm.score for bm in beams], lp_rows, b)      # l.6
         beams = [_Beam(beams[j].tokens + [v],
                        [list(lay) for lay in beams[j].cache],          # per-beam copy
@@ -99,7 +102,7 @@ def _forward_trie(model, T: Trie, M: np.ndarray, window: int):
 
 
 def trie_beam_search(model, prompt, b: int, s: int, g=1, window: int = 0,
-                     final_gc: bool = False) -> DecodeResult:
+                     final_gc: bool = False, eos=None) -> DecodeResult:
     """Alg. 2.  g = GC interval (None = never, reading R7: GC at the top of
     iteration i iff i mod g == 0).  final_gc additionally collects after the last
     append (used only for counting unique prefixes of the final hypotheses)."""
@@ -114,6 +117,8 @@ def trie_beam_search(model, prompt, b: int, s: int, g=1, window: int = 0,
             M = build_mask(T)                                # l.7
             gc_ran = True
         lp_rows = _forward_trie(model, T, M, window)         # l.9 P(x | input, M)
+        fin = [T.depth[leaf] >= t and T.token[leaf] == eos for leaf in T.leaves]
+        lp_rows = absorb_eos(lp_rows, fin, eos)              # reading R5b
         sel = select_topb(T.scores, lp_rows, b)              # l.9 argsort_b
         T.update_trie(sel)                                   # l.10
         M = update_mask(M, T, sel)                           # l.11

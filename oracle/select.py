@@ -38,3 +38,22 @@ def select_topb_np(scores, lp_rows, b: int):
     vv = np.tile(np.arange(V), J)
     order = np.lexsort((jj, vv, -cs))[: min(b, J * V)]
     return cs[order], vv[order], jj[order]
+
+
+def absorb_eos(lp_rows, finished, eos):
+    """NEXT-3, reading R5b (the paper is silent on EOS; SPEC's retire rule binds
+    only its CPU program): EOS is an ABSORBING token.  A beam whose last generated token is
+    `eos` (finished[j]) has the one-hot next-token distribution at eos (log-prob 0 there,
+    -inf elsewhere), so it stays a candidate with its score unchanged and keeps competing
+    for the b beams.  Returns the rows to select over (the others unchanged)."""
+    if eos is None:
+        return lp_rows
+    out = []
+    for lp, fin in zip(lp_rows, finished):
+        if fin:
+            row = np.full(len(lp), -np.inf)
+            row[eos] = 0.0
+            out.append(row)
+        else:
+            out.append(lp)
+    return out

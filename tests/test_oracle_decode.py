@@ -201,3 +201,82 @@ def test_memory_ratio_direction_and_bound():
         assert batch / tr.trie.N <= b * (t + s) / (t + s + b - 1) + 1e-12
         ratios.append(tr.trie.N / batch)
     assert ratios[0] > ratios[1] > ratios[2]
+
+
+
+# ---- NEXT-3: EOS as an absorbing token (reading R5b) ----------------------------------
+def _eos_seen(m, prompt, b, s):
+    """A token the no-EOS search selects at step 2 or 3 (so that EOS really occurs)."""
+    res = trie_beam_search(m, prompt, b, s, g=1)
+    return res.steps[2]["sel"][1][1]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_eos_trie_equals_batch_bitwise(seed):
+    """With EOS, trie decoding still equals batch beam search bitwise (float64)."""
+    m = _model(200 + seed, kappa=6.0, V=64)
+    prompt = [int(x) for x in synth.randint(seed, 7, 6, 64)]
+    b, s = 4, 9
+    eos = _eos_seen(m, prompt, b, s)
+    bt = batch_beam_search(m, prompt, b, s, eos=eos)
+    tr = trie_beam_search(m, prompt, b, s, g=1, eos=eos)
+    assert bt.hyps == tr.hyps
+    for sb, st in zip(bt.steps, tr.steps):
+        assert sb["sel"] == st["sel"]
+    # EOS occurred, and a finished beam only ever continues with EOS at an unchanged score
+    assert any(v == eos for (_, v, _) in tr.steps[2]["sel"] + tr.steps[3]["sel"])
+    for k in range(1, s):
+        prev = tr.steps[k - 1]["sel"]
+        for (sc, v, j) in tr.steps[k]["sel"]:
+            if prev[j][1] == eos:
+                assert v == eos and sc == prev[j][0]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_eos_never_selected_changes_nothing(seed):
+    m = _model(300 + seed, V=64)
+    prompt = [int(x) for x in synth.randint(seed, 8, 6, 64)]
+    b, s = 3, 8
+    ref = trie_beam_search(m, prompt, b, s, g=1)
+    used = {v for st in ref.steps for (_, v, _) in st["sel"]}
+    eos = min(set(range(64)) - used)
+    res = trie_beam_search(m, prompt, b, s, g=1, eos=eos)
+    assert res.hyps == ref.hyps
+
+
+def test_eos_exhaustive_special_case():
+    """b >= V^(s-1) keeps every sequence: beam search with an absorbing EOS == argmax over
+    all sequences of the absorbing chain (tokens after the first EOS are EOS, log-prob 0)."""
+    m = _model(5, V=4, kappa=3.0)
+    prompt, s, V = [1, 2, 0], 4, 4
+    for eos in range(V):
+        res = trie_beam_search(m, prompt, V ** (s - 1), s, g=1, eos=eos)
+        best_sc, best_seq = -np.inf, None
+        for seq in itertools.product(range(V), repeat=s):
+            if eos in seq:
+                e = seq.index(eos)
+                if any(x != eos for x in seq[e:]):
+                    continue  # not a sequence of the absorbing chain
+                n = e + 1      # log-probs up to and including the first EOS
+            else:
+                n = s
+            full = m.forward_full_causal(prompt + list(seq[: max(n - 1, 0)]))
+            sc = sum(full[len(prompt) - 1 + i][seq[i]] for i in range(n))
+            if sc > best_sc + 1e-12:
+                best_sc, best_seq = sc, list(seq)
+        assert abs(res.best[1] - best_sc) < 1e-9
+        assert res.best[0][len(prompt):] == best_seq
+
+
+def test_eos_all_finished_is_stable():
+    """Once every beam is finished, further steps leave the hypotheses unchanged."""
+    m = _model(12, kappa=8.0, V=32)
+    prompt = [3, 1, 4, 1, 5]
+    b = 2
+    ref = trie_beam_search(m, prompt, b, 6, g=1)
+    eos = ref.steps[1]["sel"][0][1]   # the best continuation at step 2: finishes early
+    short = trie_beam_search(m, prompt, b, 10, g=1, eos=eos)
+    longer = trie_beam_search(m, prompt, b, 14, g=1, eos=eos)
+    assert all(tok[-1] == eos for tok, _ in short.hyps)  # every beam finished by step 10
+    assert [sc for _, sc in short.hyps] == [sc for _, sc in longer.hyps]
+    assert [tok[:len(tok) - 4] for tok, _ in longer.hyps] == [tok for tok, _ in short.hyps]
