@@ -93,6 +93,7 @@ typedef struct trie_arrays {
   uint32_t* status;
   int32_t b_live; /* live beams: 1 before the first append, then b (host-tracked) */
   int32_t steps;  /* appends done since create/reset (host-tracked) */
+  uint32_t* finished; /* [R][32]: beam j's last generated token is the EOS id (trie_set_eos) */
 } trie_arrays;
 
 /* Workspace bytes for a configuration (metadata + scratch of beam_step / prune). */
@@ -195,6 +196,18 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
  */
 int trie_beam_step(trie_handle* h, const float* logits, int32_t* sel_parent_beam,
                    int32_t* sel_token, float* new_score, cudaStream_t stream);
+
+/*
+ * SURVEY §8(f) NEXT-3, EOS (reading R5b; the paper is silent): EOS is an ABSORBING
+ * token.  A beam whose last generated token is eos_id is finished: in every later
+ * trie_beam_step its next-token distribution is one-hot at eos_id (log-prob 0: one
+ * candidate, score unchanged, no logits read), so finished hypotheses keep competing for
+ * the b beams by cumulative score and a request is done when all b beams are finished
+ * (further steps leave its hypotheses unchanged).  eos_id = -1 (default) disables it.
+ * Host-side setting; EINVAL for eos_id outside [-1, V).  trie_append marks finished beams
+ * the same way; trie_create / trie_reset clear the flags.
+ */
+int trie_set_eos(trie_handle* h, int32_t eos_id);
 
 /* a-5 alone (teacher forcing): append the given selections [R][b] exactly as above. */
 int trie_append(trie_handle* h, const int32_t* sel_parent_beam, const int32_t* sel_token,

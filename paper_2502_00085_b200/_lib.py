@@ -23,7 +23,7 @@ SYMBOLS = ["trie_workspace_bytes", "trie_create", "trie_reset", "trie_destroy", 
            "trie_rope_kv_append", "trie_attn_scratch_bytes", "trie_attn_decode", "trie_beam_step",
            "trie_append", "trie_prune_compact", "trie_read_hyps", "trie_status", "trie_last_error",
            "trie_version", "trie_launch_count", "trie_attn_decode_rope", "trie_attn_plan_info",
-           "trie_batch_reorder_kv"]
+           "trie_batch_reorder_kv", "trie_set_eos"]
 
 
 class trie_cfg(ctypes.Structure):
@@ -36,7 +36,8 @@ class trie_arrays(ctypes.Structure):
     _fields_ = [("token", ctypes.c_void_p), ("parent", ctypes.c_void_p), ("depth", ctypes.c_void_p),
                 ("beam_mask", ctypes.c_void_p), ("leaf", ctypes.c_void_p), ("score", ctypes.c_void_p),
                 ("n_nodes", ctypes.c_void_p), ("prompt_len", ctypes.c_void_p),
-                ("status", ctypes.c_void_p), ("b_live", ctypes.c_int32), ("steps", ctypes.c_int32)]
+                ("status", ctypes.c_void_p), ("b_live", ctypes.c_int32), ("steps", ctypes.c_int32),
+                ("finished", ctypes.c_void_p)]
 
 
 _lib = None
@@ -73,6 +74,7 @@ def load(path: str = LIB_PATH):
         "trie_version": (ctypes.c_int, []),
         "trie_launch_count": (ctypes.c_ulonglong, []),
         "trie_batch_reorder_kv": (ctypes.c_int, [I32] * 7 + [P] * 3 + [P] * 4 + [P, P]),
+        "trie_set_eos": (ctypes.c_int, [P, I32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -182,6 +184,10 @@ def trie_prune_compact(h, k_pools, v_pools, stream=None):
     vp = (ctypes.c_void_p * max(L, 1))(*[_ptr(x) for x in v_pools])
     _check(load().trie_prune_compact(h, ctypes.cast(kp, ctypes.c_void_p), ctypes.cast(vp, ctypes.c_void_p),
                                      _stream(stream)), "trie_prune_compact")
+
+
+def trie_set_eos(h, eos_id: int):
+    _check(load().trie_set_eos(h, eos_id), "trie_set_eos")
 
 
 def trie_batch_reorder_kv(R, b, Hkv, D, cap, sel_parent_beam, prompt_len, n_rows, src_k, src_v,

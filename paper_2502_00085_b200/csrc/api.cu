@@ -106,6 +106,7 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
   char* st = take(R * b * 4);
   char* ss = take(R * b * 4);
   char* rtab = take(R * TRIE_MAX_BEAMS * (c->head_dim / 2) * 8);
+  char* fin = take(R * TRIE_MAX_BEAMS * 4);
   if (h) {
     h->token = (int32_t*)token;
     h->parent = (int32_t*)parent;
@@ -132,6 +133,7 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
     h->sel_token = (int32_t*)st;
     h->sel_score = (float*)ss;
     h->rope_tab = (float2*)rtab;
+    h->fin = (uint32_t*)fin;
     h->chunks = (int32_t)chunks;
   }
   return off;
@@ -227,6 +229,14 @@ int trie_get_arrays(const trie_handle* h, trie_arrays* o) {
   o->status = h->status;
   o->b_live = h->b_live;
   o->steps = h->steps;
+  o->finished = h->fin;
+  return TRIE_OK;
+}
+
+int trie_set_eos(trie_handle* h, int32_t eos_id) {
+  if (!h) return trie_set_error(TRIE_EINVAL, "null handle");
+  if (eos_id < -1 || eos_id >= h->cfg.vocab) return trie_set_error(TRIE_EINVAL, "eos_id not in [-1, V)");
+  h->eos = eos_id;
   return TRIE_OK;
 }
 

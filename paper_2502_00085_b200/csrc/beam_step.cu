@@ -190,7 +190,8 @@ __device__ __forceinline__ uint64_t row_key(float x, int v) {
 __device__ void append_sel(int r, int b_new, int b_old, const int* sp, const int* st,
                            const float* ss, int32_t* token, int32_t* parent, int32_t* depth,
                            uint32_t* mask, int32_t* leaf, float* score, int32_t* nn,
-                           int32_t* nkv, const int32_t* tlen, int cap, uint32_t* status) {
+                           int32_t* nkv, const int32_t* tlen, int cap, uint32_t* status,
+                           uint32_t* fin, int eos) {
   __shared__ int sm_old_leaf[TRIE_MAX_BEAMS];
   const size_t base = (size_t)r * cap;
   const int N = nn[r], t = tlen[r];
@@ -215,6 +216,7 @@ __device__ void append_sel(int r, int b_new, int b_old, const int* sp, const int
     const int slot = N + q;
     if (p < 0 || p >= N) latch(status, TRIE_ST_LEAF);
     token[base + slot] = st[q];
+    if (fin) fin[r * TRIE_MAX_BEAMS + q] = (eos >= 0 && st[q] == eos) ? 1u : 0u;  // NEXT-3
     parent[base + slot] = p;
     depth[base + slot] = (p >= 0 && p < N) ? depth[base + p] + 1 : 0;  // §3.4
     mask[base + slot] = 1u << q;
@@ -233,7 +235,7 @@ __device__ void append_sel(int r, int b_new, int b_old, const int* sp, const int
 __global__ void k_append(const int32_t* par, const int32_t* tok, const float* sc, int b_new,
                          int b_old, int32_t* token, int32_t* parent, int32_t* depth,
                          uint32_t* mask, int32_t* leaf, float* score, int32_t* nn, int32_t* nkv,
-                         const int32_t* tlen, int cap, uint32_t* status) {
+                         const int32_t* tlen, int cap, uint32_t* status, uint32_t* fin, int eos) {
   __shared__ int sp[TRIE_MAX_BEAMS], st[TRIE_MAX_BEAMS];
   __shared__ float ss[TRIE_MAX_BEAMS];
   const int r = blockIdx.x;
@@ -244,7 +246,7 @@ __global__ void k_append(const int32_t* par, const int32_t* tok, const float* sc
   }
   __syncthreads();
   append_sel(r, b_new, b_old, sp, st, ss, token, parent, depth, mask, leaf, score, nn, nkv,
-             tlen, cap, status);
+             tlen, cap, status, fin, eos);
 }
 
 // ---- the fused beam step ----------------------------------------------------------------
@@ -270,6 +272,11 @@ struct BeamStepArgs {
   float* sel_sc;
   int32_t *out_par, *out_tok;
   float* out_sc;
+  // NEXT-3 (reading R5b): EOS as an absorbing state.  A beam whose last generated token is
+  // eos (fin[r][j] != 0) continues only with eos at log-probability 0 (its row is treated
+  // as one-hot at eos: lse 0, one candidate, score unchanged); eos < 0 disables.
+  int eos;
+  uint32_t* fin;  // [R][32]
 };
 
 // element index of item i of this thread within the row
@@ -284,7 +291,8 @@ __device__ __forceinline__ int item_v(int v0, int i) {
 // sval[e]), which the candidate push reads by index.
 template <bool VEC>
 __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
-                                          const float (&val)[ITEMS], const float* sval) {
+                                          const float (&val)[ITEMS], const float* sval,
+                                          bool finrow = false) {
   __shared__ uint32_t sm_red[BS / 32], sm_tb[BS / 32];
   __shared__ float sm_sum[BS / 32];
   __shared__ __align__(16) float sm_stage[BS * ITEMS];
@@ -350,6 +358,12 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i)
       if (item_v<VEC>(v0, i) >= V) bits &= ~(1u << i);
+  }
+  if (finrow) {  // absorbing eos: the row's only candidate is eos itself
+    bits = 0u;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i)
+      if (item_v<VEC>(v0, i) == a.eos) bits |= 1u << i;
   }
   if (bits) {
     float* stg = sm_stage + threadIdx.x * ITEMS;
@@ -500,7 +514,7 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
   }
   __syncthreads();
   append_sel(r, a.b, b_live, sp, st, ss, a.token, a.parent, a.depth, a.mask, a.leaf, a.score,
-             a.nn, a.nkv, a.tlen, a.cap, a.status);
+             a.nn, a.nkv, a.tlen, a.cap, a.status, a.fin, a.eos);
 }
 
 // Register-path kernel: grid (chunks, rows), one item per CTA (any V; the TMA kernel
@@ -513,7 +527,11 @@ __global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
   const int V = a.V, v0 = c * CHUNK;
   const float* x = a.logits + (size_t)row * V;
   float val[ITEMS];
-  if (VEC) {
+  const bool finrow = a.eos >= 0 && a.fin[(row / a.b_live) * TRIE_MAX_BEAMS + row % a.b_live] != 0u;
+  if (finrow) {  // one-hot at eos (log-prob 0): no logits are read
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) val[i] = item_v<VEC>(v0, i) == a.eos ? 0.f : -INFINITY;
+  } else if (VEC) {
     const float4* x4 = reinterpret_cast<const float4*>(x);
 #pragma unroll
     for (int q = 0; q < ITEMS / 4; ++q) {
@@ -529,7 +547,7 @@ __global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
       val[i] = e < V ? __ldcs(x + e) : -INFINITY;
     }
   }
-  beam_item<VEC>(a, row, c, val, nullptr);
+  beam_item<VEC>(a, row, c, val, nullptr, finrow);
 }
 
 int launch_beam_step(trie_handle* h, const float* logits, int32_t* out_par, int32_t* out_tok,
@@ -555,6 +573,8 @@ int launch_beam_step(trie_handle* h, const float* logits, int32_t* out_par, int3
   a.status = h->status;
   a.sel_par = h->sel_parent; a.sel_tok = h->sel_token; a.sel_sc = h->sel_score;
   a.out_par = out_par; a.out_tok = out_tok; a.out_sc = out_sc;
+  a.eos = h->eos;
+  a.fin = h->fin;
   dim3 grid(a.chunks, c.n_requests * h->b_live);
   if (vec)
     launch_k(k_beam_step<true>, grid, dim3(BS), 0, s, a);
@@ -568,7 +588,8 @@ int launch_append(trie_handle* h, const int32_t* par, const int32_t* tok, const 
   const trie_cfg& c = h->cfg;
   k_append<<<c.n_requests, 256, 0, s>>>(par, tok, sc, c.beam_width, h->b_live, h->token,
                                         h->parent, h->depth, h->mask, h->leaf, h->score,
-                                        h->n_nodes, h->n_kv, h->tlen, c.capacity, h->status);
+                                        h->n_nodes, h->n_kv, h->tlen, c.capacity, h->status, h->fin,
+                                        h->eos);
   return trie_check_launch("k_append");
 }
 

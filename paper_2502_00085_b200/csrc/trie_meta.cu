@@ -39,7 +39,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total, int* sm_warp) 
 // ---- Alg. 2 l.1 initialize_trie(prompt) --------------------------------------------------
 __global__ void k_init(int32_t* token, int32_t* parent, int32_t* depth, uint32_t* mask,
                        int32_t* leaf, float* score, int32_t* nn, int32_t* nkv,
-                       const int32_t* tlen, const int32_t* prompts, int t_max, int cap) {
+                       const int32_t* tlen, const int32_t* prompts, int t_max, int cap,
+                       uint32_t* fin) {
   const int r = blockIdx.x;
   const int t = tlen[r];
   const size_t base = (size_t)r * cap;
@@ -49,6 +50,7 @@ __global__ void k_init(int32_t* token, int32_t* parent, int32_t* depth, uint32_t
     depth[base + i] = i;  // §3.4: position of the conventional sequence
     mask[base + i] = 0u;  // prompt columns are implicitly allowed for every beam
   }
+  if (threadIdx.x < TRIE_MAX_BEAMS) fin[r * TRIE_MAX_BEAMS + threadIdx.x] = 0u;  // no beam finished
   if (threadIdx.x == 0) {
     leaf[r * TRIE_MAX_BEAMS] = t - 1;
     score[r * TRIE_MAX_BEAMS] = 0.f;
@@ -61,7 +63,7 @@ int launch_init(trie_handle* h, cudaStream_t s) {
   const trie_cfg& c = h->cfg;
   k_init<<<c.n_requests, 256, 0, s>>>(h->token, h->parent, h->depth, h->mask, h->leaf, h->score,
                                       h->n_nodes, h->n_kv, h->tlen, h->prompts,
-                                      c.max_prompt_len, c.capacity);
+                                      c.max_prompt_len, c.capacity, h->fin);
   return trie_check_launch("k_init");
 }
 

@@ -20,8 +20,10 @@ def gc_due(t: int, k: int, s: int, g, final_gc: bool) -> bool:
 
 @torch.no_grad()
 def trie_beam_decode(model, st, k_pools, v_pools, prompts, lens, s, g=1, final_gc=False,
-                     record=False):
-    """Returns (hyps tokens [R][b][max_len], lens [R][b], scores [R][b], trace)."""
+                     record=False, eos=None):
+    """Returns (hyps tokens [R][b][max_len], lens [R][b], scores [R][b], trace).
+    eos: token id of an absorbing end-of-sequence (trie_set_eos, NEXT-3), None = off."""
+    st.set_eos(-1 if eos is None else int(eos))
     logits = model.prefill(prompts, lens, k_pools, v_pools, window=st.window)
     trace = []
     R, b = st.R, st.b

@@ -50,6 +50,7 @@ class TrieState:
         self.score = view(a.score, R * 32, torch.float32, (R, 32))
         self.n_nodes = view(a.n_nodes, R, torch.int32, (R,))
         self.prompt_len = view(a.prompt_len, R, torch.int32, (R,))
+        self.finished = view(a.finished, R * 32, torch.int32, (R, 32))  # uint32 flags
 
     @property
     def b_live(self) -> int:
@@ -66,6 +67,10 @@ class TrieState:
                 torch.zeros(shape, dtype=self.dtype, device=self.device))
 
     # ---- C ABI calls ----------------------------------------------------------------
+    def set_eos(self, eos_id: int):
+        """NEXT-3: EOS as an absorbing token (trie_set_eos); -1 disables."""
+        L.trie_set_eos(self.h, eos_id)
+
     def reset(self, stream=None):
         L.trie_reset(self.h, stream)
 

@@ -88,3 +88,49 @@ def test_beam_step_exact_ties_follow_total_order():
     st.beam_step(lt, par, tok)
     assert tok.cpu().numpy()[0].tolist() == [0] * 6
     assert par.cpu().numpy()[0].tolist() == [0, 1, 2, 3, 4, 5]
+
+
+
+@pytest.mark.parametrize("R,b,V", [(2, 4, 256), (2, 8, 32064), (1, 16, 128256), (2, 3, 4097)])
+def test_beam_step_absorbing_eos_matches_oracle(R, b, V):
+    """NEXT-3 (reading R5b): finished beams (last token = EOS) continue only with EOS at
+    log-prob 0.  Step 1 is steered so EOS is selected; later steps are checked against
+    beam_step_ref on the absorbed logits (finished rows one-hot at EOS), and the device
+    finished flags against the selected tokens."""
+    need_gpu()
+    from paper_2502_00085_b200.trie import TrieState
+    seed, eos = b * 13 + V, V // 3
+    prompts, lens = synth.prompts(seed, R, 6, V)
+    st = TrieState(R, b, 6, 6 + 5 * b + b, 0, 1, 1, 16, V, prompts, lens, dtype=torch.float32)
+    st.set_eos(eos)
+    scores = np.zeros((R, 1))
+    fin = np.zeros((R, 1), bool)
+    near = absorbed_rows = 0
+    for step in range(4):
+        b_live = 1 if step == 0 else b
+        logits = (synth.normal(seed, 20 + step, (R, b_live, V)) * 3.0).astype(np.float32)
+        if step in (0, 1):  # EOS is every row's argmax at steps 1 and 2
+            logits[:, :, eos] = logits.max(axis=-1) + 0.5
+        lt = torch.as_tensor(logits, device="cuda")
+        par = torch.empty(R, b, dtype=torch.int32, device="cuda")
+        tok = torch.empty_like(par)
+        sc = torch.empty(R, b, dtype=torch.float32, device="cuda")
+        st.beam_step(lt, par, tok, sc)
+        par, tok, sc = par.cpu().numpy(), tok.cpu().numpy(), sc.cpu().numpy()
+        for r in range(R):
+            absorbed = logits[r].astype(np.float64).copy()
+            for j in range(b_live):
+                if fin[r, j]:
+                    absorbed[j] = -np.inf
+                    absorbed[j, eos] = 0.0
+                    absorbed_rows += 1
+            near += _check(absorbed, scores[r], b, par[r], tok[r], sc[r])
+            for q in range(b):  # a finished parent continues with EOS at its own score
+                if fin[r, par[r, q]]:
+                    assert tok[r, q] == eos and abs(sc[r, q] - scores[r, par[r, q]]) <= 1e-6 * max(1, abs(sc[r, q]))
+        fin = tok == eos
+        assert np.array_equal(st.finished.cpu().numpy()[:, :b] != 0, fin)
+        scores = sc.astype(np.float64)
+    assert absorbed_rows > 0  # finished beams were carried through later steps
+    assert st.status() == 0
+    assert near <= 1
