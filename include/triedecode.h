@@ -202,8 +202,10 @@ int trie_beam_step(trie_handle* h, const float* logits, int32_t* sel_parent_beam
  * token.  A beam whose last generated token is eos_id is finished: in every later
  * trie_beam_step its next-token distribution is one-hot at eos_id (log-prob 0: one
  * candidate, score unchanged, no logits read), so finished hypotheses keep competing for
- * the b beams by cumulative score and a request is done when all b beams are finished
- * (further steps leave its hypotheses unchanged).  eos_id = -1 (default) disables it.
+ * the b beams by cumulative score.  A request is done when all b beams are finished: from
+ * then on trie_beam_step returns the identity selection (parent j = rank j, token eos_id,
+ * score unchanged) and appends nothing, so its trie and hypotheses stay fixed.
+ * eos_id = -1 (default) disables it.
  * Host-side setting; EINVAL for eos_id outside [-1, V).  trie_append marks finished beams
  * the same way; trie_create / trie_reset clear the flags.
  */

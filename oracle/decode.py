@@ -61,6 +61,9 @@ def batch_beam_search(model, prompt, b: int, s: int, window: int = 0, eos=None) 
     res = DecodeResult(hyps=[], best=None)
     t = len(prompt)
     for i in range(t, t + s):                                          # l.3
+        if eos is not None and len(beams) == b and all(
+                len(bm.tokens) > t and bm.tokens[-1] == eos for bm in beams):
+            break  # reading R5b: every beam finished -> decoding stops
         lp_rows = [_forward_beam(model, bm, window) for bm in beams]   # l.4-5
         fin = [len(bm.tokens) > t and bm.tokens[-1] == eos for bm in beams]
         lp_rows = absorb_eos(lp_rows, fin, eos)                        # reading R5b
@@ -111,6 +114,9 @@ def trie_beam_search(model, prompt, b: int, s: int, g=1, window: int = 0,
     t = T.t                                                  # l.3 serialize -> |input| = t
     res = DecodeResult(hyps=[], best=None)
     for i in range(t, t + s):                                # l.4
+        if eos is not None and len(T.leaves) == b and all(
+                T.depth[leaf] >= t and T.token[leaf] == eos for leaf in T.leaves):
+            break  # reading R5b: every beam finished -> decoding stops
         gc_ran = False
         if g is not None and i % g == 0:                     # l.5
             garbage_collect(T)                               # l.6

@@ -474,6 +474,27 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
 
   // ---- request stage: global top-b over b_live x k survivors ------------------------------
   const int b_live = a.b_live;
+  if (a.eos >= 0 && b_live == a.b) {  // NEXT-3: every beam finished -> the request is done:
+    // identity selection (each beam keeps its EOS-terminated hypothesis and score), no append
+    __shared__ int sm_done;
+    if (threadIdx.x == 0) {
+      int all = 1;
+      for (int j = 0; j < b_live; ++j) all &= a.fin[r * TRIE_MAX_BEAMS + j] != 0u;
+      sm_done = all;
+    }
+    __syncthreads();
+    if (sm_done) {
+      if (threadIdx.x < a.b) {
+        const int q = threadIdx.x, o2 = r * a.b + q;
+        const float scq = a.score[r * TRIE_MAX_BEAMS + q];
+        a.sel_par[o2] = q; a.sel_tok[o2] = a.eos; a.sel_sc[o2] = scq;
+        if (a.out_par) a.out_par[o2] = q;
+        if (a.out_tok) a.out_tok[o2] = a.eos;
+        if (a.out_sc) a.out_sc[o2] = scq;
+      }
+      return;
+    }
+  }
   if (threadIdx.x < b_live) sm_lse[threadIdx.x] = __ldcg(a.row_lse + r * TRIE_MAX_BEAMS + threadIdx.x);
   __syncthreads();
   // each warp takes rows w, w + 8, ...: lane = position in the row's list.  The row list

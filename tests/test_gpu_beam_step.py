@@ -105,19 +105,25 @@ def test_beam_step_absorbing_eos_matches_oracle(R, b, V):
     st.set_eos(eos)
     scores = np.zeros((R, 1))
     fin = np.zeros((R, 1), bool)
-    near = absorbed_rows = 0
-    for step in range(4):
+    near = absorbed_rows = done_seen = 0
+    for step in range(5):
         b_live = 1 if step == 0 else b
         logits = (synth.normal(seed, 20 + step, (R, b_live, V)) * 3.0).astype(np.float32)
-        if step in (0, 1):  # EOS is every row's argmax at steps 1 and 2
-            logits[:, :, eos] = logits.max(axis=-1) + 0.5
+        if step in (0, 1, 2):  # EOS is every row's argmax at steps 1-3
+            logits[:, :, eos] = logits.max(axis=-1) + 30.0
         lt = torch.as_tensor(logits, device="cuda")
         par = torch.empty(R, b, dtype=torch.int32, device="cuda")
         tok = torch.empty_like(par)
         sc = torch.empty(R, b, dtype=torch.float32, device="cuda")
+        n_before = st.n_nodes.cpu().numpy().copy()
         st.beam_step(lt, par, tok, sc)
         par, tok, sc = par.cpu().numpy(), tok.cpu().numpy(), sc.cpu().numpy()
+        n_after = st.n_nodes.cpu().numpy()
         for r in range(R):
+            if b_live == b and fin[r].all():  # done (R5b): identity selection, trie frozen
+                done_seen += 1
+                assert par[r].tolist() == list(range(b)) and (tok[r] == eos).all()
+                assert np.array_equal(sc[r], scores[r].astype(np.float32)) and n_after[r] == n_before[r]
             absorbed = logits[r].astype(np.float64).copy()
             for j in range(b_live):
                 if fin[r, j]:
@@ -132,5 +138,6 @@ def test_beam_step_absorbing_eos_matches_oracle(R, b, V):
         assert np.array_equal(st.finished.cpu().numpy()[:, :b] != 0, fin)
         scores = sc.astype(np.float64)
     assert absorbed_rows > 0  # finished beams were carried through later steps
+    assert done_seen > 0      # and some request finished all its beams
     assert st.status() == 0
     assert near <= 1
