@@ -663,7 +663,14 @@ def run_gpu(args):
     res["kv_memory"] = dict(step_in_job=int(k_star), trie_bytes=trie_b, batch_bytes=batch_b,
                             trie_peak_bytes=int(nh.sum(axis=1).max()) * kv_row,
                             ratio_batch_over_trie=round(batch_b / max(trie_b, 1), 3),
-                            bound_b_ts_over_t_s_b_1=round(b * (t + k_star) / (t + k_star + b - 1), 3))
+                            bound_b_ts_over_t_s_b_1=round(b * (t + k_star) / (t + k_star + b - 1), 3),
+                            # the Fig. 3 analog: logical KV bytes before every timed
+                            # step, trie (N rows) vs batch (b (t + k) rows per request), in MB
+                            series=dict(step_in_job=[int(k) for k in k_hist],
+                                        trie_MB=[round(float(nh[i].sum()) * kv_row / 1e6, 1)
+                                                 for i in range(len(k_hist))],
+                                        batch_MB=[round(R * (b if k > 0 else 1) * (t + k) * kv_row / 1e6, 1)
+                                                  for k in k_hist]))
     if not args.no_e2e:
         res["e2e"] = run_e2e(hp, args, world)
     if world > 1:
