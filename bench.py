@@ -206,9 +206,16 @@ class HotPath:
                 self._gather(d["out"])
         if events is not None and fused:
             events[0][1].record()
+        if events is not None:  # the last two pairs: beam step (a-4/a-5/a-2), GC (a-6)
+            events[-2][0].record()
         st.beam_step(d["logits"], self.sel_p, self.sel_t, self.sel_s)
+        if events is not None:
+            events[-2][1].record()
+            events[-1][0].record()
         if gc:
             st.prune_compact(self.kp, self.vp)
+        if events is not None:
+            events[-1][1].record()
 
     def _gather(self, out):
         from paper_2502_00085_b200.dist import gather_heads
@@ -227,7 +234,7 @@ class HotPath:
                     for timed in (False, True):
                         evs = None
                         if timed:
-                            n_pairs = 1 if self.fused[var] else self.L
+                            n_pairs = (1 if self.fused[var] else self.L) + 2
                             evs = [(torch.cuda.Event(enable_timing=True, external=True),
                                     torch.cuda.Event(enable_timing=True, external=True))
                                    for _ in range(n_pairs)]
@@ -554,17 +561,20 @@ def run_gpu(args):
     end_ev = [torch.cuda.Event() for _ in range(2)]
 
     attn_step = []  # (step index, k in job) per harvested launch; bytes computed afterwards
+    beam_ms, gc_ms = [], []  # per instrumented step: trie_beam_step, trie_prune_compact
 
     def harvest(slot):
         var_p, kj_p, i_p = pending.pop(slot)
         end_ev[slot].synchronize()  # only step i_p; step i_p + 1 keeps the GPU busy
         evs = hp.ev[(var_p, slot)]  # var_p = (variant, gc) key
-        per = hp.L // len(evs)  # fused: one pair spans the L attention launches of the step
-        for e0, e1 in evs:
+        per = hp.L // (len(evs) - 2)  # fused: one pair spans the L attention launches of the step
+        for e0, e1 in evs[:-2]:
             dt = e0.elapsed_time(e1)
             for _ in range(per):
                 attn_ms.append(dt / per)
                 attn_step.append((i_p, kj_p))
+        beam_ms.append(evs[-2][0].elapsed_time(evs[-2][1]))
+        gc_ms.append(evs[-1][0].elapsed_time(evs[-1][1]))
 
     # Region A (value): plain step graphs back to back.
     t0.record(stream)
@@ -646,6 +656,13 @@ def run_gpu(args):
                            in_step=dict(achieved=round(in_step_gbs, 1),
                                         avg_launch_us=round(float(np.mean(attn_ms)) * 1e3, 2),
                                         attn_share_of_step=round(float(np.sum(attn_ms)) / ms_b, 4),
+                                        breakdown_ms_per_step=dict(
+                                            attn=round(float(np.sum(attn_ms)) / args.steps, 4),
+                                            beam_step=round(float(np.mean(beam_ms)), 4),
+                                            gc=round(float(np.mean(gc_ms)), 4),
+                                            step=round(ms_b / args.steps, 4),
+                                            note="region B event nodes; the model GEMMs are context "
+                                                 "and not in the step (SURVEY §8(d))"),
                                         timing="CUDA event nodes around every attention launch of "
                                                f"{args.steps} instrumented step graphs "
                                                f"({ms_b / args.steps:.3f} ms/step; includes the "

@@ -95,6 +95,7 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
   char* prompts = take(R * c->max_prompt_len * 4);
   char* newidx = take(R * cap * 4);
   char* moves = take(R * cap * 4);
+  char* mdst = take(R * cap * 4);
   char* nmoves = take(R * 4);
   char* cmax = take(R * b * chunks * 4);
   char* csum = take(R * b * chunks * 4);
@@ -121,6 +122,7 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
     h->prompts = (int32_t*)prompts;
     h->newidx = (int32_t*)newidx;
     h->moves = (int32_t*)moves;
+    h->moves_dst = (int32_t*)mdst;
     h->n_moves = (int32_t*)nmoves;
     h->chunk_max = (float*)cmax;
     h->chunk_sum = (float*)csum;

@@ -25,7 +25,8 @@ struct trie_handle {
   int32_t* prompts = nullptr; // [R][t_max]
   // prune scratch
   int32_t* newidx = nullptr;  // [R][cap]
-  int32_t* moves = nullptr;   // [R][cap]
+  int32_t* moves = nullptr;   // [R][cap] source slots of the moved K/V rows (ascending)
+  int32_t* moves_dst = nullptr;  // [R][cap] their destination slots
   int32_t* n_moves = nullptr; // [R]
   // beam-step scratch
   float* chunk_max = nullptr;     // [R][b][chunks]

@@ -77,7 +77,7 @@ constexpr int PRUNE_BS = 512;
 __global__ void __launch_bounds__(PRUNE_BS) k_prune_scan(
     int32_t* token, int32_t* parent, int32_t* depth, uint32_t* mask, int32_t* leaf,
     int32_t* nn, const int32_t* nkv, const int32_t* tlen, int32_t* newidx, int32_t* moves,
-    int32_t* n_moves, int b_live, int cap, uint32_t* status) {
+    int32_t* moves_dst, int32_t* n_moves, int b_live, int cap, uint32_t* status) {
   __shared__ int sm_warp[32];
   pdl_trigger();
   pdl_wait();
@@ -128,7 +128,10 @@ __global__ void __launch_bounds__(PRUNE_BS) k_prune_scan(
       depth[base + dst] = dep;
       mask[base + dst] = msk;
     }
-    if (mv) moves[base + mcarry + mpre] = n;
+    if (mv) {
+      moves[base + mcarry + mpre] = n;
+      moves_dst[base + mcarry + mpre] = dst;
+    }
     mcarry += mtot;
     __syncthreads();
   }
@@ -145,37 +148,41 @@ __global__ void __launch_bounds__(PRUNE_BS) k_prune_scan(
 }
 
 // ---- §3.5 Compaction of the KV cache (the paper's index_select) -----------------
-// One CTA per (request, layer); all KV heads of a moved slot are copied with 16-byte
-// vectors.  Moves are applied in ascending batches (read-all, barrier, write-all) for
-// the same in-place safety argument as above.
+// One CTA per (request, layer, group of hg KV heads): the K and V rows of the moved slots
+// of those heads (regions no other CTA touches), 16-byte vectors, (source, destination)
+// pairs written by k_prune_scan so a copy is two dependent loads deep.  hg keeps the grid
+// near 4096 CTAs (r61: one head per CTA cut Llama's GC 40 -> 25 us per step but made Phi's
+// 32-head launch of 65k CTAs slower, 44 -> 78 us).  Moves are applied in ascending
+// batches (read-all, barrier, write-all) for the same in-place safety argument as above;
+// a few moved rows per request (r08 ncu: ~9 on Llama) fit one batch.
 struct PoolPtrs {
   void* k[TRIE_MAX_LAYERS];
   void* v[TRIE_MAX_LAYERS];
 };
 
-constexpr int COMPACT_BS = 256;
+constexpr int COMPACT_BS = 128;
 constexpr int COMPACT_VEC = 4;  // 16-byte vectors in flight per thread per batch
 __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant__ PoolPtrs pp,
                                                            const int32_t* moves,
-                                                           const int32_t* n_moves,
-                                                           const int32_t* newidx, int Hkv,
-                                                           int row_bytes, int cap) {
+                                                           const int32_t* moves_dst,
+                                                           const int32_t* n_moves, int Hkv,
+                                                           int hg, int row_bytes, int cap) {
   pdl_trigger();
   pdl_wait();
-  const int r = blockIdx.x, layer = blockIdx.y;
+  const int r = blockIdx.x, layer = blockIdx.y, h0 = blockIdx.z * hg;
   const int nm = n_moves[r];
   if (nm == 0) return;
+  const int nh = min(hg, Hkv - h0);
   const size_t base = (size_t)r * cap;
-  const int vec_per_row = row_bytes / 16;                // one (head, slot) row
-  const int vec_per_slot = 2 * Hkv * vec_per_row;       // K and V, all heads
-  char* kb = (char*)pp.k[layer] + (size_t)r * Hkv * cap * row_bytes;
-  char* vb = (char*)pp.v[layer] + (size_t)r * Hkv * cap * row_bytes;
+  const int vpr = row_bytes / 16;  // 16-byte vectors per (head, slot) row
+  const size_t hoff = ((size_t)r * Hkv + h0) * cap * row_bytes;
+  const size_t hstride = (size_t)cap * row_bytes;
+  char* kb = (char*)pp.k[layer] + hoff;
+  char* vb = (char*)pp.v[layer] + hoff;
   const int per_batch = COMPACT_BS * COMPACT_VEC;
-  const long total = (long)nm * vec_per_slot;
+  const int per_slot = 2 * nh * vpr;
+  const long total = (long)nm * per_slot;
   for (long b0 = 0; b0 < total; b0 += per_batch) {
-    // batches must not split a slot's reads from an earlier slot's writes in a racy way:
-    // all reads of the batch happen before all its writes (barrier below); batches are
-    // ascending in move order, so later reads never hit earlier-written targets' sources.
     int4 val[COMPACT_VEC];
     char* dstp[COMPACT_VEC];
 #pragma unroll
@@ -183,17 +190,15 @@ __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant
       const long e = b0 + (long)u * COMPACT_BS + threadIdx.x;
       dstp[u] = nullptr;
       if (e < total) {
-        const int mi = (int)(e / vec_per_slot);
-        int rem = (int)(e % vec_per_slot);
-        const int kv = rem / (Hkv * vec_per_row);
-        rem -= kv * Hkv * vec_per_row;
-        const int hh = rem / vec_per_row, c = rem % vec_per_row;
-        const int src = moves[base + mi];
-        const int dst = newidx[base + src];
-        char* pool = kv ? vb : kb;
-        const size_t hoff = (size_t)hh * cap * row_bytes + (size_t)c * 16;
-        val[u] = *(const int4*)(pool + hoff + (size_t)src * row_bytes);
-        dstp[u] = pool + hoff + (size_t)dst * row_bytes;
+        const int mi = (int)(e / per_slot);
+        int rem = (int)(e % per_slot);
+        const int kv = rem / (nh * vpr);
+        rem -= kv * nh * vpr;
+        const int hh = rem / vpr, c = rem % vpr;
+        const int src = moves[base + mi], dst = moves_dst[base + mi];
+        char* pool = (kv ? vb : kb) + (size_t)hh * hstride;
+        val[u] = *(const int4*)(pool + (size_t)src * row_bytes + (size_t)c * 16);
+        dstp[u] = pool + (size_t)dst * row_bytes + (size_t)c * 16;
       }
     }
     __syncthreads();
@@ -208,7 +213,7 @@ int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t 
   const trie_cfg& c = h->cfg;
   launch_k(k_prune_scan, dim3(c.n_requests), dim3(PRUNE_BS), 0, s, h->token, h->parent, h->depth,
            h->mask, h->leaf, h->n_nodes, (const int32_t*)h->n_kv, (const int32_t*)h->tlen, h->newidx,
-           h->moves, h->n_moves, h->b_live, c.capacity, h->status);
+           h->moves, h->moves_dst, h->n_moves, h->b_live, c.capacity, h->status);
   int rc = trie_check_launch("k_prune_scan");
   if (rc) return rc;
   if (c.n_layers == 0 || kp == nullptr) return TRIE_OK;
@@ -218,10 +223,14 @@ int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t 
     pp.v[l] = vp[l];
   }
   const int esz = c.kv_dtype == TRIE_BF16 ? 2 : 4;
-  dim3 grid(c.n_requests, c.n_layers);
+  const long units = (long)c.n_requests * c.n_layers * c.n_kv_heads;
+  int hg = (int)((units + 4095) / 4096);
+  if (hg > c.n_kv_heads) hg = c.n_kv_heads;
+  if (hg < 1) hg = 1;
+  dim3 grid(c.n_requests, c.n_layers, (c.n_kv_heads + hg - 1) / hg);
   launch_k(k_kv_compact, grid, dim3(COMPACT_BS), 0, s, pp, (const int32_t*)h->moves,
-           (const int32_t*)h->n_moves, (const int32_t*)h->newidx, c.n_kv_heads, c.head_dim * esz,
-           c.capacity);
+           (const int32_t*)h->moves_dst, (const int32_t*)h->n_moves, c.n_kv_heads, hg,
+           c.head_dim * esz, c.capacity);
   return trie_check_launch("k_kv_compact");
 }
 
