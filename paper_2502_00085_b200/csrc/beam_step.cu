@@ -541,7 +541,11 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
 // Register-path kernel: grid (chunks, rows), one item per CTA (any V; the TMA kernel
 // below needs V % 4 == 0 and 16-byte aligned rows).
 template <bool VEC>
-__global__ void __launch_bounds__(BS, 4) k_beam_step(const BeamStepArgs a) {
+#ifndef TRIE_BEAM_MINB
+#define TRIE_BEAM_MINB 4  // CTAs per SM the register budget is sized for (64 regs, small spill):
+                          // r64 microbench, Llama shape: 4 -> 41.2 us, 3 -> 47.5, 2 -> 62.4
+#endif
+__global__ void __launch_bounds__(BS, TRIE_BEAM_MINB) k_beam_step(const BeamStepArgs a) {
   pdl_trigger();
   pdl_wait();
   const int c = blockIdx.x, row = blockIdx.y;
