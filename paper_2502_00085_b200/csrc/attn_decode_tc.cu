@@ -396,7 +396,11 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
 // =========================================================================================
 template <int D, int MT, int RS = 1>
 struct WideCfg {
+#ifdef TRIE_WIDE_STAGES  // experiment builds only
+  static constexpr int STAGES = TRIE_WIDE_STAGES;
+#else
   static constexpr int STAGES = D >= 128 ? 3 : 4;
+#endif
   using RG = Ring<D, STAGES>;
   static constexpr int KS = D / 16;
   static constexpr int DT = D / 8;
