@@ -36,6 +36,9 @@ struct AttnParams {
   // griddepcontrol.wait: the first ring stages fill while the predecessor drains.
   int pre_tiles;
   int half_tiles;         // narrow / wide: the last tile of an item loads 32-row boxes when <= 32 rows remain
+  // NEXT-3 (narrow / wide, handle path with an EOS id): fin [R][32] finished flags; a
+  // request whose b_live beams are all finished is done -- its CTAs read and write nothing
+  const uint32_t* fin;
 };
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);

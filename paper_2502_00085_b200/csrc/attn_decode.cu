@@ -186,6 +186,9 @@ __global__ void __launch_bounds__(128) k_attn_combine(const AttnParams p) {
   if (gw >= total) return;
   const int m = gw % Qg, h = (gw / Qg) % p.Hkv, r = gw / (Qg * p.Hkv);
   const int D = p.D;
+  if (p.fin != nullptr &&  // NEXT-3: a finished request's splits wrote nothing; neither do we
+      __all_sync(0xffffffffu, lane >= p.b_live || p.fin[r * TRIE_MAX_BEAMS + lane] != 0u))
+    return;
   const float* base = p.part + (((size_t)r * p.Hkv + h) * p.splits * Qg) * (D + 2);
   // lanes own splits (<= 64): (m_s, l_s) loaded in parallel, weights w_s = 2^(m_s - M)
   float ms[2], ls[2];

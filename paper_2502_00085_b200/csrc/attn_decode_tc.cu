@@ -138,6 +138,8 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     if constexpr (ROPE) if (lane != 0)
       append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane, app_done,
                             it.N - p.b_live);
+    if (it.done && lane == 0)  // no tile is consumed: let the pre-wait loads land before exit
+      for (int i = 0; i < npre; ++i) mbar_wait(&full[i], 0u);
     ATTN_TRC(lane == 0, 5);
     return;
   }
@@ -331,6 +333,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   ATTN_TRC(lane == 0, 3);
+  if (it.done) return;  // NEXT-3: finished request, output not written
   // ---- epilogue: column sums over the 8 lanes of a column quad, transpose via smem ----
 #pragma unroll
   for (int nq = 0; nq < NQ; ++nq)
@@ -486,6 +489,8 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr, INT_MAX,
                                   npre, INT_MAX, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
     }
+    if (it.done && lane == 0)  // no tile is consumed: let the pre-wait loads land before exit
+      for (int i = 0; i < npre; ++i) mbar_wait(&full[i], 0u);
     ATTN_TRC(lane == 0, 5);
     return;
   }
@@ -706,6 +711,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       }
     }
   }
+  if (it.done) return;  // NEXT-3: finished request, output not written
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int m = qm[u];

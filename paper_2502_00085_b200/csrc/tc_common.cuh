@@ -108,6 +108,7 @@ struct Ring {
 
 struct ItemInfo {
   int tile0, ntiles, lo, N, t, fast_from;
+  int done;  // NEXT-3: every beam of the request finished (no tiles, no output)
 };
 
 // Whole warp 0 (lane 0 writes *info): tile range of this (r, split) and the first tile
@@ -156,9 +157,13 @@ __device__ __forceinline__ void item_setup(const AttnParams& p, int r, int split
   const int total = (N + TC_TR - 1) / TC_TR - first;
   const int per = (total + p.splits - 1) / p.splits;
   const int tb = min(total, split * per), te = min(total, (split + 1) * per);
+  // NEXT-3: a request whose live beams have all finished (EOS) is done -- skip it
+  const bool done = p.fin != nullptr &&
+                    __all_sync(0xffffffffu, lane >= p.b_live || p.fin[r * TRIE_MAX_BEAMS + lane] != 0u);
   if (lane == 0) {
+    info->done = done ? 1 : 0;
     info->tile0 = first + tb;
-    info->ntiles = te - tb;
+    info->ntiles = done ? 0 : te - tb;
     info->lo = lo;
     info->N = N;
     info->t = t;

@@ -240,3 +240,57 @@ def _fuzz_cases(n=24, seed=2502):
 def test_fused_fuzz_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W, ragged, steps, rho):
     """trie_attn_decode_rope on seeded random shapes vs the oracle (bf16, 2e-2)."""
     _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=ragged, steps=steps, rho=rho)
+
+
+@pytest.mark.parametrize("Hq,Hkv,D", [(8, 8, 96), (32, 4, 128)])   # narrow (Qg 4), wide (Qg 32)
+def test_fused_skips_finished_requests(Hq, Hkv, D):
+    """NEXT-3 (reading R5b): with an EOS id set, trie_attn_decode_rope skips a request whose
+    beams are all finished (no append, output rows untouched); the other requests are
+    computed as usual (vs the oracle)."""
+    need_gpu()
+    from paper_2502_00085_b200.trie import TrieState
+    R, b, t, V, steps, eos, base = 3, 4, 200, 300, 4, 7, 500000.0
+    seed = 4242 + D
+    prompts, lens = synth.prompts(seed, R, t, V)
+    sels = per_request_selections(seed, R, steps, b, V, 0.5)
+    # request 1 finishes every beam at the last step: tokens = eos
+    sels[-1][1][1, :] = eos
+    for k in range(steps - 1):
+        sels[k][1][sels[k][1] == eos] = eos + 1
+    cap = (t + b * steps + b + 63) // 64 * 64
+    st = TrieState(R, b, t, cap, 1, Hq, Hkv, D, V, prompts, lens, dtype=torch.bfloat16)
+    st.set_eos(eos)
+    kp, vp = st.new_pools()
+    for par, tok in sels:
+        st.append(torch.as_tensor(par, device="cuda"), torch.as_tensor(tok, device="cuda"))
+        st.prune_compact(kp, vp)
+    fin = st.finished.cpu().numpy()[:, :b] != 0
+    assert fin[1].all() and not fin[0].all() and not fin[2].all()
+    tries = build_tries(prompts, lens, sels, b, g=1, final_gc=True)
+    K = torch.as_tensor(synth.normal(seed, 1, (R, Hkv, cap, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
+    Vv = torch.as_tensor(synth.normal(seed, 2, (R, Hkv, cap, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
+    kp[0].copy_(K)
+    vp[0].copy_(Vv)
+    q = torch.as_tensor(synth.normal(seed, 3, (R, b, Hq, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
+    kn = torch.as_tensor(synth.normal(seed, 4, (R, b, Hkv, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
+    vn = torch.as_tensor(synth.normal(seed, 5, (R, b, Hkv, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
+    out = torch.full_like(q, 123.0)
+    st.attn_decode_rope(q, kn, vn, kp[0], vp[0], base, out, rows_hint=t + steps)
+    torch.cuda.synchronize()
+    assert st.status() == 0
+    o = out.float().cpu().numpy()
+    assert (o[1] == 123.0).all()                               # skipped: output untouched
+    assert torch.equal(kp[0][1].cpu(), K[1].cpu())             # and nothing appended
+    Kh, Vh = K.float().cpu().numpy().astype(np.float64), Vv.float().cpu().numpy().astype(np.float64)
+    q0, k0, v0 = (x.float().cpu().numpy().astype(np.float64) for x in (q, kn, vn))
+    for r in (0, 2):
+        T = tries[r]
+        Kr, Vr = Kh[r].copy(), Vh[r].copy()
+        qr = np.zeros((b, Hq, D))
+        for j, leaf in enumerate(T.leaves):
+            pos = T.depth[leaf]
+            qr[j] = rope_rotate_half(q0[r, j], pos, base)
+            Kr[:, leaf] = rope_rotate_half(k0[r, j], pos, base)
+            Vr[:, leaf] = v0[r, j]
+        o_ref, _ = attn_ref(qr, Kr[:, :T.N], Vr[:, :T.N], T)
+        assert rel_err(o[r], o_ref) <= 2e-2
