@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import types
 import os
 import subprocess
 import sys
@@ -147,6 +148,14 @@ class HotPath:
             for slot in range(self.NB):
                 qkv = torch.randn(L * per_layer, device=dev, generator=gen).to(torch.bfloat16)
                 lg = torch.randn(R * bl * V, device=dev, generator=lgen) * 3.0
+                if wl.get("eos_frac", 0.0) > 0.0 and var == "steady":
+                    # NEXT-3 experiment (--eos-frac f): EOS (token 0) is the argmax of every
+                    # row of the first round(f R) requests, so they finish at their second
+                    # step and are done from the third on; the others never emit it
+                    nf = int(round(wl["eos_frac"] * R))
+                    lg3 = lg.view(R, bl, V)
+                    lg3[:nf, :, 0] = lg3[:nf].amax(dim=-1) + 30.0
+                    lg3[nf:, :, 0] = -30.0
                 views = []
                 for l in range(L):
                     base = l * per_layer
@@ -165,6 +174,8 @@ class HotPath:
         self.sel_t = torch.empty_like(self.sel_p)
         self.sel_s = torch.empty(R, b, dtype=torch.float32, device=dev)
         self.rows_hint = t + s
+        if wl.get("eos_frac", 0.0) > 0.0:
+            self.st.set_eos(0)
         self.g = int(wl.get("g", 1))  # GC interval (Alg. 2); 1 on the hot path
         self.graphs = {}
         self.launches_per_graph = {}
@@ -297,6 +308,9 @@ class HotPath:
         torch.cuda.synchronize()
         g = self.attn_graph
         g.replay()
+        done = None
+        if self.wl.get("eos_frac"):  # NEXT-3: requests whose beams all finished are skipped
+            done = (self.st.finished.cpu().numpy()[:, :self.b] != 0).all(axis=1)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -305,7 +319,7 @@ class HotPath:
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / (reps * L)
-        return us, self.attn_bytes(self.k, self.live_rows())
+        return us, self.attn_bytes(self.k, self.live_rows(), None if done is None else ~done)
 
     def live_rows(self):
         """Per request: rows some live beam can see (prompt + generated nodes with a
@@ -318,10 +332,15 @@ class HotPath:
         t = self.st.prompt_len.cpu().numpy()
         return np.array([t[r] + int(np.count_nonzero(m[r, t[r]:N[r]])) for r in range(self.R)])
 
-    def attn_bytes(self, k_in_job, N):
+    def attn_bytes(self, k_in_job, N, live=None):
         """Algorithmic bytes of one trie_attn_decode launch: unique
-        KV rows U_r x 2*Hkv*D*2 + Q and O (bf16) + mask/depth words of generated rows."""
+        KV rows U_r x 2*Hkv*D*2 + Q and O (bf16) + mask/depth words of generated rows.
+        live: optional [R] bool -- requests still decoding (NEXT-3: done requests, all
+        beams finished at EOS, are skipped by the kernels and move no bytes)."""
         t, b, W, R, Hq, Hkv, D = self.t, self.b, self.W, self.R, self.Hq, self.Hkv, self.D
+        if live is not None and not np.all(live):
+            sub = types.SimpleNamespace(t=t, b=b, W=W, R=int(np.sum(live)), Hq=Hq, Hkv=Hkv, D=D)
+            return HotPath.attn_bytes(sub, k_in_job, np.asarray(N)[np.asarray(live, bool)])
         bl = 1 if k_in_job == 0 else b
         if k_in_job == 0:
             N = np.full(R, t)
@@ -526,6 +545,7 @@ def run_gpu(args):
     if args.requests:
         wl["R"] = args.requests
     wl["g"] = args.gc_interval
+    wl["eos_frac"] = args.eos_frac
     if wl.get("kv_shard") and world > 1 and backend != "nccl":
         raise SystemExit("the KV-head shard's per-layer all-gather is captured in CUDA graphs: NCCL only")
     hp = HotPath(wl, rank, dev, world)
@@ -614,7 +634,13 @@ def run_gpu(args):
         harvest(slot)
     ms_b = t2.elapsed_time(t3)
     nh_all = n_hist_b.cpu().numpy()
-    attn_bytes = [hp.attn_bytes(kj, nh_all[i]) for i, kj in attn_step]
+    def live_at(kj):  # NEXT-3 experiment: the first round(f R) requests are done from job step 2
+        if not wl.get("eos_frac") or kj < 2:
+            return None
+        lv = np.ones(R, bool)
+        lv[: int(round(wl["eos_frac"] * R))] = False
+        return lv
+    attn_bytes = [hp.attn_bytes(kj, nh_all[i], live_at(kj)) for i, kj in attn_step]
     st_bits = hp.st.status()
     assert st_bits == 0, f"device status bits {st_bits:#x}"
     in_step_gbs = float(np.sum(attn_bytes) / (np.sum(attn_ms) * 1e-3) / 1e9)
@@ -638,6 +664,7 @@ def run_gpu(args):
                            new_tokens=s, layers=L, q_heads_per_gpu=hp.Hq, kv_heads_per_gpu=hp.Hkv,
                            head_dim=hp.D,
                            vocab=hp.V, window=hp.W, gc_interval=hp.g,
+                           **({"eos_frac": wl["eos_frac"]} if wl.get("eos_frac") else {}),
                            parallelism=(f"kv-head-shard{world} (per-layer all-gather of attention outputs)"
                                         if hp.kv_shard else f"request-dp{world}"),
                            execution="cuda-graph replay per step",
@@ -865,6 +892,8 @@ def main():
                     help="Alg. 2's GC interval g (1 = every step, the hot path; 0 = never)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference", "batch"],
                     help="ours | reference (CPU oracle) | batch (GPU batch beam search, NEXT-2)")
+    ap.add_argument("--eos-frac", type=float, default=0.0,
+                    help="NEXT-3 experiment: EOS id 0 finishes this fraction of the requests early")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
