@@ -205,7 +205,7 @@ int trie_beam_step(trie_handle* h, const float* logits, int32_t* sel_parent_beam
  * the b beams by cumulative score.  A request is done when all b beams are finished: from
  * then on trie_beam_step returns the identity selection (parent j = rank j, token eos_id,
  * score unchanged) and appends nothing, so its trie and hypotheses stay fixed; the fused
- * trie_attn_decode_rope (narrow / wide kernels) then skips the request entirely -- no K/V
+ * trie_attn_decode_rope then skips the request entirely -- no K/V
  * append, its output rows are NOT written (their logits are never read again).
  * eos_id = -1 (default) disables it.
  * Host-side setting; EINVAL for eos_id outside [-1, V).  trie_append marks finished beams

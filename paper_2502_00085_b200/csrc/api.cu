@@ -435,8 +435,8 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.aux = scratch;
   p.part = (float*)((char*)scratch + pl.counter_bytes);
   p.splits = pl.splits;
-  // NEXT-3: with an EOS id, the narrow / wide kernels skip requests whose beams all finished
-  if (h->eos >= 0 && !trie::attn_umma_eligible(p)) p.fin = h->fin;
+  // NEXT-3: with an EOS id, the fused kernels skip requests whose beams all finished
+  if (h->eos >= 0) p.fin = h->fin;
   if (cfg->window == 0 && prefetch_enabled()) {
     // tiles below the shortest prompt's last row hold prompt rows that no kernel of the
     // library writes (AttnParams::pre_tiles); row t - 1 is excluded: it is the first

@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
       const int j = beam, ii = row % g;
       constexpr int HD = D / 2;
       const int c0 = grp * HD;
-      if (!trc) {
+      if (!trc && !it.done) {  // NEXT-3: a done request (all beams finished) writes nothing
         if (p.splits == 1) {
           __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
           const float inv = l > 0.f ? 1.f / l : 0.f;

@@ -242,7 +242,7 @@ def test_fused_fuzz_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W, ragged, ste
     _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=ragged, steps=steps, rho=rho)
 
 
-@pytest.mark.parametrize("Hq,Hkv,D", [(8, 8, 96), (32, 4, 128)])   # narrow (Qg 4), wide (Qg 32)
+@pytest.mark.parametrize("Hq,Hkv,D", [(8, 8, 96), (32, 4, 128), (32, 2, 128)])  # narrow, wide, tcgen05
 def test_fused_skips_finished_requests(Hq, Hkv, D):
     """NEXT-3 (reading R5b): with an EOS id set, trie_attn_decode_rope skips a request whose
     beams are all finished (no append, output rows untouched); the other requests are
