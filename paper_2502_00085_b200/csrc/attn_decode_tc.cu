@@ -145,8 +145,11 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
   }
   // ===== consumer warp =====
   // Waits for the item setup BEFORE loading Q: overlapping the two (as k_attn_wide does)
-  // measured 4.5% slower on the Phi workload (r34 A/B, 16.01k vs 16.76k request-steps/s).
+  // measured 4.5% slower on the Phi workload (r34 A/B, 16.01k vs 16.76k request-steps/s;
+  // re-checked r72 with TRIE_NARROW_QOVERLAP builds: 16.91k vs 17.56k).
+#ifndef TRIE_NARROW_QOVERLAP  // experiment builds: load Q while warp 0 runs the setup
   asm volatile("bar.sync 2, 64;" ::: "memory");  // item setup published by warp 0
+#endif
   const int g = p.Hq / p.Hkv, Qg = p.b_live * g;
   const int gq = lane >> 2, cq = lane & 3;
   const size_t mbase = (size_t)r * p.cap;
@@ -201,6 +204,9 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       }
     }
   }
+#ifdef TRIE_NARROW_QOVERLAP
+  asm volatile("bar.sync 2, 64;" ::: "memory");
+#endif
   const ItemInfo it = *info;
   float o[C::DM][NQ][4];
 #pragma unroll
