@@ -145,3 +145,52 @@ def test_bench_two_ranks_request_dp():
     res = json.loads([l for l in out.stdout.strip().splitlines() if l.startswith("{")][-1])
     assert res["n_gpus"] == 2 and res["value"] > 0 and res["scaling"] == "weak"
     assert res["config"]["parallelism"] == "request-dp2"
+
+
+@pytest.mark.parametrize("seed,Hkv,b,R", [(0, 4, 3, 2), (7, 1, 8, 2), (3, 2, 4, 3)])
+def test_gpu_batch_beam_search_equals_gpu_trie_decode(seed, Hkv, b, R):
+    """The paper's equivalence on the GPU, end to end on the tiny decoder
+    (fp32): batch beam search (Alg. 1) built from the library's calls -- private
+    single-beam caches per beam, trie_beam_step for the top-b, trie_batch_reorder_kv for
+    the cache reorder -- selects exactly what the trie decode selects at every step."""
+    need_gpu()
+    from paper_2502_00085_b200 import _lib
+    from paper_2502_00085_b200.decode import trie_beam_decode
+    from paper_2502_00085_b200.model import TinyModel
+    from paper_2502_00085_b200.trie import TrieState
+    t, s, V, D = 8, 12, 256, 16
+    prompts, lens = synth.prompts(seed, R, t, V)
+    gm = TinyModel(seed, Hkv=Hkv)
+    st = TrieState(R, b, t, t + b * s + b, 2, 4, Hkv, D, V, prompts, lens, dtype=torch.float32)
+    kp, vp = st.new_pools()
+    _, _, _, trace = trie_beam_decode(gm, st, kp, vp, prompts, lens, s, g=1, record=True)
+    # batch beam search: R*b single-beam chains (prompt replicated), two pool sets
+    rep = np.repeat(prompts, b, axis=0)
+    rlen = np.repeat(lens, b)
+    ccap = t + s + 1
+    ch = TrieState(R * b, 1, t, ccap, 2, 4, Hkv, D, V, rep, rlen, dtype=torch.float32)
+    sel = TrieState(R, b, t, t + b * s + b, 0, 4, Hkv, D, V, prompts, lens, dtype=torch.float32)
+    P = [ch.new_pools(), ch.new_pools()]
+    logits = gm.prefill(rep, rlen, P[0][0], P[0][1])
+    P[1][0].copy_(P[0][0])
+    P[1][1].copy_(P[0][1])
+    zeros = torch.zeros(R * b, dtype=torch.int32, device="cuda")
+    cur = 0
+    for k in range(1, s + 1):
+        lg = logits.view(R, b, V)
+        if k == 1:
+            lg = lg[:, :1].contiguous()  # one live beam: the prompt
+        sp = torch.empty(R, b, dtype=torch.int32, device="cuda")
+        tk = torch.empty_like(sp)
+        sc = torch.empty(R, b, dtype=torch.float32, device="cuda")
+        sel.beam_step(lg, sp, tk, sc)
+        _lib.trie_batch_reorder_kv(R, b, Hkv, D, ccap, sp, ch.prompt_len, ch.n_nodes,
+                                   list(P[cur][0]), list(P[cur][1]), list(P[1 - cur][0]), list(P[1 - cur][1]))
+        ch.append(zeros, tk.view(-1))
+        cur = 1 - cur
+        assert sp.cpu().numpy().tolist() == trace[k - 1]["par"].tolist(), f"step {k}: parents differ"
+        assert tk.cpu().numpy().tolist() == trace[k - 1]["tok"].tolist(), f"step {k}: tokens differ"
+        np.testing.assert_allclose(sc.cpu().numpy(), trace[k - 1]["score"], rtol=1e-4, atol=1e-4)
+        if k < s:
+            logits = gm.step(ch, P[cur][0], P[cur][1])
+    assert ch.status() == 0 and sel.status() == 0
