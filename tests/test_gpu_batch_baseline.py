@@ -147,8 +147,9 @@ def test_bench_two_ranks_request_dp():
     assert res["config"]["parallelism"] == "request-dp2"
 
 
-@pytest.mark.parametrize("seed,Hkv,b,R", [(0, 4, 3, 2), (7, 1, 8, 2), (3, 2, 4, 3)])
-def test_gpu_batch_beam_search_equals_gpu_trie_decode(seed, Hkv, b, R):
+@pytest.mark.parametrize("seed,Hkv,b,R,use_eos", [(0, 4, 3, 2, False), (7, 1, 8, 2, False), (3, 2, 4, 3, False),
+                                                   (0, 4, 3, 2, True), (2, 4, 5, 2, True)])
+def test_gpu_batch_beam_search_equals_gpu_trie_decode(seed, Hkv, b, R, use_eos):
     """The paper's equivalence on the GPU, end to end on the tiny decoder
     (fp32): batch beam search (Alg. 1) built from the library's calls -- private
     single-beam caches per beam, trie_beam_step for the top-b, trie_batch_reorder_kv for
@@ -163,13 +164,19 @@ def test_gpu_batch_beam_search_equals_gpu_trie_decode(seed, Hkv, b, R):
     gm = TinyModel(seed, Hkv=Hkv)
     st = TrieState(R, b, t, t + b * s + b, 2, 4, Hkv, D, V, prompts, lens, dtype=torch.float32)
     kp, vp = st.new_pools()
-    _, _, _, trace = trie_beam_decode(gm, st, kp, vp, prompts, lens, s, g=1, record=True)
+    eos = None
+    if use_eos:  # NEXT-3: an EOS id the trie decode selects at step 3 (absorbing, R5b)
+        _, _, _, tr0 = trie_beam_decode(gm, st, kp, vp, prompts, lens, 3, g=1, record=True)
+        eos = int(tr0[2]["tok"][0, 0])
+        st.reset()
+    _, _, _, trace = trie_beam_decode(gm, st, kp, vp, prompts, lens, s, g=1, record=True, eos=eos)
     # batch beam search: R*b single-beam chains (prompt replicated), two pool sets
     rep = np.repeat(prompts, b, axis=0)
     rlen = np.repeat(lens, b)
     ccap = t + s + 1
     ch = TrieState(R * b, 1, t, ccap, 2, 4, Hkv, D, V, rep, rlen, dtype=torch.float32)
     sel = TrieState(R, b, t, t + b * s + b, 0, 4, Hkv, D, V, prompts, lens, dtype=torch.float32)
+    sel.set_eos(-1 if eos is None else eos)
     P = [ch.new_pools(), ch.new_pools()]
     logits = gm.prefill(rep, rlen, P[0][0], P[0][1])
     P[1][0].copy_(P[0][0])
