@@ -312,13 +312,20 @@ class HotPath:
         if self.wl.get("eos_frac"):  # NEXT-3: requests whose beams all finished are skipped
             done = (self.st.finished.cpu().numpy()[:, :self.b] != 0).all(axis=1)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
+        # one event per replay boundary (back to back, no host sync in between): the mean
+        # over all reps * L launches, and the spread of the per-replay means
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+        evs[0].record()
+        for i in range(reps):
             g.replay()
-        e1.record()
+            evs[i + 1].record()
         torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / (reps * L)
+        per = np.array([evs[i].elapsed_time(evs[i + 1]) * 1e3 / L for i in range(reps)])
+        us = evs[0].elapsed_time(evs[-1]) * 1e3 / (reps * L)
+        self.attn_spread = dict(replays=reps, launches=reps * L,
+                                p10_us=round(float(np.percentile(per, 10)), 2),
+                                median_us=round(float(np.median(per)), 2),
+                                p90_us=round(float(np.percentile(per, 90)), 2))
         return us, self.attn_bytes(self.k, self.live_rows(), None if done is None else ~done)
 
     def live_rows(self):
@@ -675,6 +682,7 @@ def run_gpu(args):
                            unit="GB/s", frac=round(ach / peak, 4), frac_of_8TBps=round(ach / 8000, 4),
                            traffic=_traffic(args.workload, R, b), peak_source=peak_src,
                            avg_launch_us=round(c_us, 2), bytes_per_launch=int(c_bytes),
+                           launch_us_spread=hp.attn_spread,
                            kernel_launch=("trie_attn_decode_rope (fused a-1 + a-3; bytes counted: a-3 only)"
                                           if hp.fused["steady"] else "trie_attn_decode"),
                            timing=(f"CUDA events around a graph of the step's {hp.L} attention launches "
