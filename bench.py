@@ -64,16 +64,18 @@ def _peaks():
 class Clocks:
     """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
 
+    QUERY = ("--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
     def __init__(self, gpu_index: int):
         self.proc = None
+        self.gpu_index = gpu_index
         self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}_{gpu_index}.csv")
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={gpu_index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", f"--id={gpu_index}", self.QUERY, "--format=csv,noheader,nounits",
+                 "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -91,6 +93,17 @@ class Clocks:
             f = [x.strip() for x in line.split(",")]
             if len(f) >= 7 and f[0].isdigit():
                 rows.append(f)
+        post = False
+        if not rows:  # the sampler had not started writing yet: one query right at the end
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu_index}", self.QUERY,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=10).stdout
+                rows = [[x.strip() for x in line.split(",")] for line in out.splitlines()
+                        if line.strip() and line.split(",")[0].strip().isdigit()]
+                post = True
+            except Exception:
+                rows = []
         if not rows:
             return None
         sm = [int(r[0]) for r in rows]
@@ -100,8 +113,11 @@ class Clocks:
             for n, v in zip(names, r[3:7]):
                 if v.lower() == "active":
                     reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]),
-                "reasons": sorted(reasons), "samples": len(rows)}
+        res = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]),
+               "reasons": sorted(reasons), "samples": len(rows)}
+        if post:
+            res["sampled"] = "once, right after the timed regions"
+        return res
 
 
 # ------------------------------------------------------------------------------------------
@@ -612,7 +628,6 @@ def run_gpu(args):
         launches += hp.launches_per_graph[(var, i % 2, False)]
     t1.record(stream)
     torch.cuda.synchronize()
-    clk = clocks.stop()
     ms = t0.elapsed_time(t1)
     if world > 1:
         tt = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
@@ -656,6 +671,8 @@ def run_gpu(args):
     # between CUDA events on the launching stream -- kernel time without the event-node
     # latency that region B's per-launch events add
     c_us, c_bytes = hp.attn_only_timing(reps=max(4, min(20, 2 * args.steps)))
+    # clocks sampled across regions A, B and C (contiguous GPU work, 100 ms period)
+    clk = clocks.stop()
     ach = c_bytes / (c_us * 1e-6) / 1e9
     peak, peak_src = _peaks()
 
