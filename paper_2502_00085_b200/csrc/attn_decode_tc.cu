@@ -119,14 +119,19 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     }
 #endif
     if constexpr (ROPE) {
-      // fill the ring first (tiles that hold no leaf), then lane 0 streams the rest while
-      // lanes 1..31 append the leaves' K/V rows
+      // lane 0 fills the ring with leaf-free tiles while lanes 1..31 append the leaves' K/V
+      // rows; after the reconvergence lane 0 streams the rest, the append already done (no
+      // reliance on the scheduler interleaving a spinning lane 0 with the append; r81:
+      // timing-neutral vs appending after lane 0's stream)
       const int first_leaf = it.N - p.b_live;
       int fill = min(C::STAGES, it.ntiles);
       while (fill > npre && (it.tile0 + fill) * TC_TR > first_leaf) --fill;
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr,
                                     INT_MAX, npre, fill, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
+      else
+        append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane,
+                              app_done, first_leaf);
       __syncwarp();
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
@@ -135,9 +140,6 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr, INT_MAX,
                                   npre, INT_MAX, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
     }
-    if constexpr (ROPE) if (lane != 0)
-      append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane, app_done,
-                            it.N - p.b_live);
     if (it.done && lane == 0)  // no tile is consumed: let the pre-wait loads land before exit
       for (int i = 0; i < npre; ++i) mbar_wait(&full[i], 0u);
     ATTN_TRC(lane == 0, 5);
@@ -484,13 +486,13 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr,
                                     INT_MAX, npre, fill, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
+      else
+        append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane,
+                              app_done, first_leaf);
       __syncwarp();
       if (lane == 0)
         producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, app_done,
                                     first_leaf, max(fill, npre), INT_MAX, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
-      else
-        append_leaves_rope<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + it.ntiles) * TC_TR, lane,
-                              app_done, first_leaf);
     } else if (lane == 0) {
       producer_loop<D, C::STAGES>(&kmap, &vmap, p, r, h, it, ring, full, empty, nullptr, INT_MAX,
                                   npre, INT_MAX, nullptr, p.half_tiles ? &kmh : nullptr, &vmh);
