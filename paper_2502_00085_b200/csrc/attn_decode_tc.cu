@@ -183,25 +183,28 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
       const __nv_bfloat16* src = nullptr;
       if (m < Qg) src = q + (((size_t)r * p.b_live + m / g) * p.Hq + h * g + m % g) * D;
 #pragma unroll
-      for (int ks = 0; ks < C::KS; ++ks) {
+      for (int ks = 0; ks < C::KS; ++ks)
 #pragma unroll
-        for (int hi = 0; hi < 2; ++hi) {
-          const int d = ks * 16 + hi * 8 + cq * 2;
-          uint32_t v = src ? *(const uint32_t*)(src + d) : 0u;
-          if constexpr (ROPE) {
-            if (src) {  // rotate-half at the beam's depth, rounded to bf16 like trie_rope_kv_append
-              const int pd = d < HALF ? d + HALF : d - HALF;
-              const uint32_t pv = *(const uint32_t*)(src + pd);
-              const float2 x = __bfloat1622float2(*(const __nv_bfloat162*)&v);
-              const float2 xp = __bfloat1622float2(*(const __nv_bfloat162*)&pv);
-              const int i0 = d % HALF, j = m / g;
-              const float2* tab = p.rope_tab + ((size_t)r * p.b_live + j) * HALF;
-              const float2 c0 = tab[i0], c1 = tab[i0 + 1];
-              const float sg = d < HALF ? -1.f : 1.f;
-              v = pack_bf16(x.x * c0.x + sg * xp.x * c0.y, x.y * c1.x + sg * xp.y * c1.y);
+        for (int hi = 0; hi < 2; ++hi)
+          qb[nq][ks][hi] = src ? *(const uint32_t*)(src + ks * 16 + hi * 8 + cq * 2) : 0u;
+      if constexpr (ROPE) {
+        // rotate-half at the beam's depth, rounded to bf16 like trie_rope_kv_append: the
+        // partner of column c < D/2 is c + D/2, held by this thread in k-step ks + KS/2 (as in
+        // k_attn_wide; r83: rotating with per-element partner loads cost ~3 us per Phi launch)
+        static_assert(C::KS % 2 == 0, "head_dim must be a multiple of 32 for the fused RoPE");
+        if (src) {
+          const int j = m / g;
+#pragma unroll
+          for (int ks = 0; ks < C::KS / 2; ++ks)
+#pragma unroll
+            for (int hi = 0; hi < 2; ++hi) {
+              const int col = ks * 16 + hi * 8 + cq * 2;  // < D/2
+              const float4 tt = __ldg((const float4*)(p.rope_tab + ((size_t)r * p.b_live + j) * HALF + col));
+              const float2 x1 = __bfloat1622float2(*(const __nv_bfloat162*)&qb[nq][ks][hi]);
+              const float2 x2 = __bfloat1622float2(*(const __nv_bfloat162*)&qb[nq][ks + C::KS / 2][hi]);
+              qb[nq][ks][hi] = pack_bf16(x1.x * tt.x - x2.x * tt.y, x1.y * tt.z - x2.y * tt.w);
+              qb[nq][ks + C::KS / 2][hi] = pack_bf16(x2.x * tt.x + x1.x * tt.y, x2.y * tt.z + x1.y * tt.w);
             }
-          }
-          qb[nq][ks][hi] = v;
         }
       }
     }
