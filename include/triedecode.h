@@ -112,7 +112,8 @@ int trie_create(const trie_cfg* cfg, void* workspace, size_t workspace_bytes,
                 const int32_t* prompt_lens_host, const int32_t* prompt_tokens,
                 trie_handle** out, cudaStream_t stream);
 
-/* Re-initialise the metadata from the stored prompts (same as trie_create, async). */
+/* Re-initialise the metadata from the stored prompts (same as trie_create, async; the
+ * latched status word is cleared too). */
 int trie_reset(trie_handle* h, cudaStream_t stream);
 
 int trie_destroy(trie_handle* h);
@@ -145,13 +146,16 @@ int trie_rope_kv_append(trie_handle* h, void* q, void* k_new, const void* v_new,
  * q, out: [R][b_live][Hq][D]; lse (optional, may be NULL): [R][b_live][Hq] float,
  * natural-log sum of exp of the scaled scores.  rows_hint: expected max N over requests
  * (sizes the split-K grid; 0 = capacity).  scratch: >= trie_attn_scratch_bytes().
+ * status (optional device word, may be NULL): TRIE_ST_EMPTY_ROW is OR-ed in when a query
+ * row has no allowed key (its output row is then 0 and its lse -inf).
  */
 size_t trie_attn_scratch_bytes(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint);
 int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const void* k_pool,
                      const void* v_pool, const int32_t* prompt_len, const int32_t* parent,
                      const int32_t* depth, const int32_t* leaf_ids, const int32_t* n_nodes,
                      const uint32_t* beam_mask, int32_t window, int32_t rows_hint, void* out,
-                     float* lse, void* scratch, size_t scratch_bytes, cudaStream_t stream);
+                     float* lse, void* scratch, size_t scratch_bytes, uint32_t* status,
+                     cudaStream_t stream);
 
 /*
  * Which attention kernel a configuration uses (host only): info_host[0] = path (0 CUDA-core

@@ -18,7 +18,9 @@ Modules
   trie        -- trie state, Alg. 3 mask, update_trie / update_mask, GC (§3.5)
   decode      -- Alg. 1 batch beam search, Alg. 2 trie beam search, greedy
   kernels_ref -- kernel-level pure functions the GPU path is compared against:
-                 attn_ref, beam_step_ref, append_ref, prune_compact_ref, mask_ref
+                 build_tries (teacher-forced Alg. 2 l.10-11 + §3.5 GC: the append,
+                 bitset and prune/compaction reference), mask_bits / soa (Alg. 3 mask
+                 packed per node), attn_ref (§3.3), beam_step_ref (Alg. 2 l.9)
 
 Parity pins: tests/test_oracle_*.py (marker "not gpu").  Every function here is pinned;
 there is no "parity unpinned" function.

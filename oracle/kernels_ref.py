@@ -10,7 +10,7 @@ import numpy as np
 
 from .numerics import log_softmax
 from .select import select_topb_np
-from .trie import Trie, build_mask, garbage_collect, update_mask, window_allow
+from .trie import Trie, build_mask, garbage_collect, window_allow
 
 
 # ---- integer path ----------------------------------------------------------------------
@@ -108,12 +108,3 @@ def beam_step_ref(logits, scores, b: int):
     k = min(b, J * Vv)
     gap = (cs[k - 1] - cs[k]) if len(cs) > k else np.inf
     return jj[:k].astype(np.int32), vv[:k].astype(np.int32), cs[:k], gap, lp
-
-
-def append_ref(T: Trie, parent_beam, token, scores=None):
-    """Alg. 2 l.10-11 on a copy of the mask: update_trie then update_mask."""
-    sel = [(0.0 if scores is None else float(scores[i]), int(token[i]), int(parent_beam[i]))
-           for i in range(len(token))]
-    M = build_mask(T)
-    T.update_trie(sel)
-    return update_mask(M, T, sel)

@@ -62,7 +62,7 @@ def load(path: str = LIB_PATH):
         "trie_rope_kv_append": (ctypes.c_int, [P, P, P, P, P, P, ctypes.c_float, P]),
         "trie_attn_scratch_bytes": (SZ, [CP, I32, I32]),
         "trie_attn_decode": (ctypes.c_int, [CP, I32, P, P, P, P, P, P, P, P, P, I32, I32, P, P, P,
-                                            SZ, P]),
+                                            SZ, P, P]),
         "trie_attn_decode_rope": (ctypes.c_int, [P, P, P, P, P, P, ctypes.c_float, I32, P, P, P, SZ, P]),
         "trie_attn_plan_info": (ctypes.c_int, [CP, I32, I32, P]),
         "trie_beam_step": (ctypes.c_int, [P, P, P, P, P, P]),
@@ -152,12 +152,13 @@ def trie_attn_scratch_bytes(cfg: trie_cfg, b_live: int, rows_hint: int = 0) -> i
 
 
 def trie_attn_decode(cfg, b_live, q, k_pool, v_pool, prompt_len, parent, depth, leaf_ids, n_nodes,
-                     beam_mask, window, rows_hint, out, lse, scratch, stream=None):
+                     beam_mask, window, rows_hint, out, lse, scratch, stream=None, status=None):
     sb = 0 if scratch is None else scratch.numel() * scratch.element_size()
     _check(load().trie_attn_decode(ctypes.byref(cfg), b_live, _ptr(q), _ptr(k_pool), _ptr(v_pool),
                                    _ptr(prompt_len), _ptr(parent), _ptr(depth), _ptr(leaf_ids),
                                    _ptr(n_nodes), _ptr(beam_mask), window, rows_hint, _ptr(out),
-                                   _ptr(lse), _ptr(scratch), sb, _stream(stream)), "trie_attn_decode")
+                                   _ptr(lse), _ptr(scratch), sb, _ptr(status), _stream(stream)),
+           "trie_attn_decode")
 
 
 def trie_attn_decode_rope(h, q, k_new, v_new, k_pool, v_pool, rope_theta, rows_hint, out, lse, scratch,

@@ -44,6 +44,9 @@ static int validate(const trie_cfg* c) {
     return trie_set_error(TRIE_EINVAL, "n_layers not in [0, %d]", TRIE_MAX_LAYERS);
   if (c->n_q_heads < 1 || c->n_kv_heads < 1 || c->n_q_heads % c->n_kv_heads)
     return trie_set_error(TRIE_EINVAL, "n_q_heads %% n_kv_heads != 0 (GQA, S:104)");
+  if (c->beam_width * (c->n_q_heads / c->n_kv_heads) > 128)
+    return trie_set_error(TRIE_EINVAL, "beam_width * (n_q_heads / n_kv_heads) = %d > 128 queries per KV head",
+                          c->beam_width * (c->n_q_heads / c->n_kv_heads));
   if (c->head_dim < 16 || c->head_dim > 256 || c->head_dim % 16)
     return trie_set_error(TRIE_EINVAL, "head_dim must be a multiple of 16 in [16, 256]");
   if (c->window < 0) return trie_set_error(TRIE_EINVAL, "window < 0");
@@ -210,6 +213,8 @@ int trie_reset(trie_handle* h, cudaStream_t stream) {
   h->b_live = 1;
   h->steps = 0;
   h->rope_tab_steps = -1;
+  const cudaError_t e = cudaMemsetAsync(h->status, 0, 4, stream);  // a new job: clear latched faults
+  if (e != cudaSuccess) return trie_set_error(TRIE_ECUDA, "trie_reset: %s", cudaGetErrorString(e));
   return trie::launch_init(h, stream);
 }
 
@@ -280,12 +285,11 @@ static size_t part_bytes(const trie_cfg* c, int b_live, int splits) {
   return (size_t)c->n_requests * c->n_kv_heads * splits * Qg * (c->head_dim + 2) * 4;
 }
 
-// Attention plan: persistent tensor-core path (default for bf16, D in {64, 96, 128},
-// b_live*g <= 128) or the per-item paths; split count; scratch layout
-// [queue/item counters | split partials | derived beam mask].  A pure function of the
-// shapes, so trie_attn_scratch_bytes and trie_attn_decode agree.
+// Attention plan: split count and scratch layout [counters | split partials | derived
+// beam mask].  A pure function of the shapes, so trie_attn_scratch_bytes and
+// trie_attn_decode agree.  (The opt-in persistent work-queue kernel of r08 was slower
+// everywhere and is kept only as profiles/r08_experiments/attn_persist.patch.)
 struct AttnPlan {
-  bool persist;
   int splits;
   size_t counter_bytes, part_bytes, mask_bytes;
 };
@@ -296,13 +300,7 @@ static AttnPlan attn_plan(const trie_cfg* c, int b_live, int rows_hint, bool rop
   trie::AttnParams sp = shape_params(c, b_live);
   sp.rope = rope ? 1 : 0;
   sp.rows_hint = rows;
-  pl.persist = trie::attn_persist_enabled() && trie::attn_tc_shape_ok(sp);
-  if (pl.persist) {
-    pl.splits = trie::attn_persist_splits(sp, rows, sm_count());
-    pl.counter_bytes = align_up(trie::attn_persist_counter_bytes(sp));
-  } else {
-    pl.splits = trie::attn_plan_splits(sp, rows, sm_count());
-  }
+  pl.splits = trie::attn_plan_splits(sp, rows, sm_count());
   pl.part_bytes = align_up(part_bytes(c, b_live, pl.splits));
   pl.mask_bytes = align_up((size_t)c->n_requests * c->capacity * 4);
   return pl;
@@ -310,15 +308,21 @@ static AttnPlan attn_plan(const trie_cfg* c, int b_live, int rows_hint, bool rop
 
 size_t trie_attn_scratch_bytes(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint) {
   if (validate(cfg)) return 0;
+  // the larger of the plain plan (+ the derived mask of beam_mask == NULL) and the fused
+  // trie_attn_decode_rope plan: the kernels of the two may differ in occupancy
   const AttnPlan pl = attn_plan(cfg, b_live, rows_hint);
-  return pl.counter_bytes + pl.part_bytes + pl.mask_bytes + 256;
+  const AttnPlan pr = attn_plan(cfg, b_live, rows_hint, true);
+  const size_t a = pl.counter_bytes + pl.part_bytes + pl.mask_bytes;
+  const size_t b = pr.counter_bytes + pr.part_bytes;
+  return (a > b ? a : b) + 256;
 }
 
 int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const void* k_pool,
                      const void* v_pool, const int32_t* prompt_len, const int32_t* parent,
                      const int32_t* depth, const int32_t* leaf_ids, const int32_t* n_nodes,
                      const uint32_t* beam_mask, int32_t window, int32_t rows_hint, void* out,
-                     float* lse, void* scratch, size_t scratch_bytes, cudaStream_t stream) {
+                     float* lse, void* scratch, size_t scratch_bytes, uint32_t* status,
+                     cudaStream_t stream) {
   int rc = validate(cfg);
   if (rc) return rc;
   if (b_live < 1 || b_live > cfg->beam_width) return trie_set_error(TRIE_EINVAL, "b_live");
@@ -352,11 +356,11 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
   p.mask = beam_mask;
   p.aux = scratch;
   p.part = (float*)((char*)scratch + pl.counter_bytes);
-  p.status = nullptr;
+  p.status = status;
   p.window = window;
   p.splits = pl.splits;
   if (trie::attn_tc_supported(p))
-    return pl.persist ? trie::launch_attn_persist(p, stream) : trie::launch_attn_tc(p, stream);
+    return trie::launch_attn_tc(p, stream);
   return trie::launch_attn_v1(p, stream);
 }
 
@@ -372,9 +376,9 @@ int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,
   const int Qg = b_live * (cfg->n_q_heads / cfg->n_kv_heads);
   int path = 0;
   if (trie::attn_tc_shape_ok(p))
-    path = pl.persist ? 4 : trie::attn_umma_eligible(p) ? 3 : (Qg <= 16 ? 1 : 2);
+    path = trie::attn_umma_eligible(p) ? 3 : (Qg <= 16 ? 1 : 2);
   p.k = p.v = (const void*)(uintptr_t)256;  // aligned placeholders for the shape test
-  const bool fused = !pl.persist && trie::attn_rope_fusable(p);
+  const bool fused = trie::attn_rope_fusable(p);
   info_host[0] = path;
   info_host[1] = fused ? attn_plan(cfg, b_live, rows_hint, true).splits : pl.splits;
   info_host[2] = fused ? 1 : 0;
@@ -410,7 +414,7 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.k_new = k_new;
   p.v_new = v_new;
   p.rope_tab = h->rope_tab;
-  const bool fuse = !trie::attn_persist_enabled() && trie::attn_rope_fusable(p) &&
+  const bool fuse = trie::attn_rope_fusable(p) &&
                     (((uintptr_t)q | (uintptr_t)k_new | (uintptr_t)v_new) & 3) == 0;
   if (!fuse) {  // two launches: rotate + append, then attention over the handle's trie
     int rc = trie::launch_rope_append(h, const_cast<void*>(q), const_cast<void*>(k_new), v_new,
@@ -418,7 +422,7 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
     if (rc) return rc;
     return trie_attn_decode(cfg, b_live, q, k_pool, v_pool, h->tlen, h->parent, h->depth, h->leaf,
                             h->n_nodes, h->mask, cfg->window, rows_hint, out, lse, scratch,
-                            scratch_bytes, stream);
+                            scratch_bytes, h->status, stream);
   }
   if (h->rope_tab_steps != h->steps || h->rope_tab_theta != rope_theta ||
       h->rope_tab_blive != b_live) {  // once per step, shared by all layers

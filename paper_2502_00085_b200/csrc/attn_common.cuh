@@ -16,7 +16,7 @@ struct AttnParams {
   const int32_t* nn;      // [R]
   const uint32_t* mask;   // [R][cap]
   float* part;            // split partials
-  void* aux;              // persistent path: zero-initialised queue / item counters
+  void* aux;              // scratch base (counters, if any, precede the split partials)
   uint32_t* status;
   int R, b_live, Hq, Hkv, D, cap, window, splits;
   int rows_hint;          // expected rows per request (planning only; 0 = capacity)
@@ -47,13 +47,9 @@ bool attn_rope_fusable(const AttnParams& p);
 bool attn_tc_supported(const AttnParams& p);
 int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s);
 int attn_plan_splits(const AttnParams& p, int rows_est, int sms);
-bool attn_persist_enabled();
 bool attn_tc_shape_ok(const AttnParams& p);
 bool attn_umma_eligible(const AttnParams& p);
 int attn_umma_occ(const AttnParams& p);
 int launch_attn_umma(const AttnParams& p, cudaStream_t s);
-int attn_persist_splits(const AttnParams& p, int rows_est, int sms);
-size_t attn_persist_counter_bytes(const AttnParams& p);
-int launch_attn_persist(const AttnParams& p, cudaStream_t s);
 
 }  // namespace trie

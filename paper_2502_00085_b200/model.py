@@ -89,9 +89,12 @@ class TinyModel:
         return out
 
     @torch.no_grad()
-    def step(self, st, k_pools, v_pools):
+    def step(self, st, k_pools, v_pools, fused=False, hook=None):
         """One decode forward of the b_live leaves: context GEMMs around the library's
-        trie_rope_kv_append + trie_attn_decode.  Returns logits [R][b_live][V] fp32."""
+        trie_rope_kv_append + trie_attn_decode (fused=True: the one-launch
+        trie_attn_decode_rope).  hook(layer, q, k, v, o), if given, sees every layer's
+        un-rotated projections and the attention output.  Returns logits [R][b_live][V]
+        fp32."""
         R, b = st.R, st.b_live
         leaf = st.leaf[:, :b].long()
         tok = torch.gather(st.token.long(), 1, leaf)  # tokens of the pending leaves
@@ -101,9 +104,14 @@ class TinyModel:
             q = (h @ lw["wq"]).view(R, b, self.Hq, self.D).contiguous()
             k = (h @ lw["wk"]).view(R, b, self.Hkv, self.D).contiguous()
             v = (h @ lw["wv"]).view(R, b, self.Hkv, self.D).contiguous()
-            st.rope_kv_append(q, k, v, k_pools[l], v_pools[l], self.base)
             o = torch.empty_like(q)
-            st.attn_decode(q, k_pools[l], v_pools[l], o)
+            if fused:
+                st.attn_decode_rope(q, k, v, k_pools[l], v_pools[l], self.base, o)
+            else:
+                st.rope_kv_append(q, k, v, k_pools[l], v_pools[l], self.base)
+                st.attn_decode(q, k_pools[l], v_pools[l], o)
+            if hook is not None:
+                hook(l, q, k, v, o)
             x = x + o.view(R * b, -1) @ lw["wo"]
             x = self._mlp(x, lw)
         return self._logits(x).view(R, b, self.V)

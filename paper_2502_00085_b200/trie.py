@@ -51,6 +51,7 @@ class TrieState:
         self.n_nodes = view(a.n_nodes, R, torch.int32, (R,))
         self.prompt_len = view(a.prompt_len, R, torch.int32, (R,))
         self.finished = view(a.finished, R * 32, torch.int32, (R, 32))  # uint32 flags
+        self.status_word = view(a.status, 1, torch.int32, (1,))         # TRIE_ST_* bits
 
     @property
     def b_live(self) -> int:
@@ -82,12 +83,12 @@ class TrieState:
         b_live = self.b_live
         need = L.trie_attn_scratch_bytes(self.cfg, b_live, rows_hint)
         if self.attn_scratch is None or self.attn_scratch.numel() < need:
-            # zero-initialised once: the persistent kernel's queue counters live here and
-            # every launch leaves them at zero
+            # zero-initialised once (counters in the scratch are left at zero by every launch)
             self.attn_scratch = torch.zeros(need, dtype=torch.uint8, device=self.device)
         L.trie_attn_decode(self.cfg, b_live, q, k_pool_l, v_pool_l, self.prompt_len, self.parent,
                            self.depth, self.leaf, self.n_nodes, self.beam_mask if use_mask else None,
-                           self.window, rows_hint, out, lse, self.attn_scratch, stream)
+                           self.window, rows_hint, out, lse, self.attn_scratch, stream,
+                           status=self.status_word)
 
     def attn_decode_rope(self, q, k_new, v_new, k_pool_l, v_pool_l, rope_theta, out, lse=None,
                          rows_hint=0, stream=None):

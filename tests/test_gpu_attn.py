@@ -294,3 +294,56 @@ def test_fused_skips_finished_requests(Hq, Hkv, D):
             Vr[:, leaf] = v0[r, j]
         o_ref, _ = attn_ref(qr, Kr[:, :T.N], Vr[:, :T.N], T)
         assert rel_err(o[r], o_ref) <= 2e-2
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_empty_row_latches_status(dt):
+    """TRIE_ST_EMPTY_ROW (S:54 "an all-blocked row signals a trie/mask construction bug"):
+    a beam whose own mask bit is missing, under a window of 1 key (self only, reading R14),
+    has no allowed key -- the pure trie_attn_decode latches the bit in the caller's status
+    word, the row's lse is -inf and its output row 0; the other beam's row is unaffected."""
+    need_gpu()
+    from paper_2502_00085_b200 import _lib
+    t, b, Hq, Hkv, D = 4, 2, 4, 2, 64
+    dtype = torch.bfloat16 if dt == "bf16" else torch.float32
+    cfg = _lib.make_cfg(1, b, t, 64, 1, Hq, Hkv, D, 100, 1, 1,
+                        _lib.TRIE_BF16 if dt == "bf16" else _lib.TRIE_F32)
+    cu = lambda x: torch.as_tensor(np.asarray(x), device="cuda")  # noqa: E731
+    parent = cu(np.array([[-1, 0, 1, 2, 3, 3] + [-1] * 58], np.int32))
+    depth = cu(np.array([[0, 1, 2, 3, 4, 4] + [0] * 58], np.int32))
+    mask = cu(np.array([[0, 0, 0, 0, 1, 0] + [0] * 58], np.int32))  # slot 5: beam 1's bit missing
+    leaf = cu(np.array([[4, 5] + [0] * 30], np.int32))
+    K = torch.randn(1, Hkv, 64, D, device="cuda").to(dtype)
+    Vv = torch.randn(1, Hkv, 64, D, device="cuda").to(dtype)
+    Q = torch.randn(1, b, Hq, D, device="cuda").to(dtype)
+    out = torch.full_like(Q, 7.0)
+    lse = torch.zeros(1, b, Hq, device="cuda")
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    scratch = torch.zeros(_lib.trie_attn_scratch_bytes(cfg, b, 6), dtype=torch.uint8, device="cuda")
+    _lib.trie_attn_decode(cfg, b, Q, K, Vv, cu(np.array([t], np.int32)), parent, depth, leaf,
+                          cu(np.array([6], np.int32)), mask, 1, 6, out, lse, scratch, status=status)
+    torch.cuda.synchronize()
+    assert int(status.item()) & _lib.TRIE_ST_EMPTY_ROW
+    l = lse.cpu().numpy()
+    assert np.isneginf(l[0, 1]).all() and np.isfinite(l[0, 0]).all()
+    assert (out[0, 1].float() == 0).all()
+    # beam 0 (window 1: itself only) reads exactly V[slot 4]
+    ref = Vv[0, :, 4].float().repeat_interleave(Hq // Hkv, dim=0)
+    assert torch.allclose(out[0, 0].float(), ref, atol=1e-2 if dt == "bf16" else 1e-5)
+
+
+def test_leaf_latch_and_reset_clears_status():
+    """TRIE_ST_LEAF: a leaf id outside [0, N) (a corrupted handle) latches on the next beam
+    step; trie_reset starts a new job with a clear status word."""
+    need_gpu()
+    from paper_2502_00085_b200 import _lib
+    from paper_2502_00085_b200.trie import TrieState
+    prompts, lens = synth.prompts(5, 1, 6, 50)
+    st = TrieState(1, 3, 6, 40, 0, 1, 1, 16, 50, prompts, lens, dtype=torch.float32)
+    st.beam_step(torch.randn(1, 1, 50, device="cuda"))
+    assert st.status() == 0
+    st.leaf[0, 1] = 9999
+    st.beam_step(torch.randn(1, 3, 50, device="cuda"))
+    assert st.status() & _lib.TRIE_ST_LEAF
+    st.reset()
+    assert st.status() == 0

@@ -244,12 +244,12 @@ def test_eos_never_selected_changes_nothing(seed):
     assert res.hyps == ref.hyps
 
 
-def test_eos_exhaustive_special_case():
+def _eos_exhaustive(s, eos_ids):
     """b >= V^(s-1) keeps every sequence: beam search with an absorbing EOS == argmax over
     all sequences of the absorbing chain (tokens after the first EOS are EOS, log-prob 0)."""
     m = _model(5, V=4, kappa=3.0)
-    prompt, s, V = [1, 2, 0], 3, 4
-    for eos in (0, 2, 3):
+    prompt, V = [1, 2, 0], 4
+    for eos in eos_ids:
         res = trie_beam_search(m, prompt, V ** (s - 1), s, g=1, eos=eos)
         best_sc, best_seq = -np.inf, None
         for seq in itertools.product(range(V), repeat=s):
@@ -266,6 +266,16 @@ def test_eos_exhaustive_special_case():
                 best_sc, best_seq = sc, list(seq)
         assert abs(res.best[1] - best_sc) < 1e-9
         assert res.best[0][len(prompt):] == best_seq
+
+
+def test_eos_exhaustive_special_case():
+    _eos_exhaustive(3, (0, 2, 3))
+
+
+@pytest.mark.slow
+def test_eos_exhaustive_special_case_s4_all_ids():
+    """The full pin (s = 4, b = V^3 = 64, every token id as EOS): ~40 s of CPU."""
+    _eos_exhaustive(4, range(4))
 
 
 def test_eos_all_finished_is_stable():
