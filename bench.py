@@ -120,6 +120,40 @@ class Clocks:
         return res
 
 
+METRIC = "beam-decode steps/s (request-steps/s, hot path) + trie-attn HBM GB/s"
+
+
+def _workload(args):
+    wl = dict(WORKLOADS[args.workload])
+    if args.beam:
+        wl["b"] = args.beam
+    if args.requests:
+        wl["R"] = args.requests
+    wl["g"] = args.gc_interval
+    wl["eos_frac"] = args.eos_frac
+    return wl
+
+
+def _scaling(wl):
+    return "strong" if wl.get("kv_shard") else "weak"
+
+
+def bench_config(wl, world):
+    """The `config` object of the JSON line (both arms): the workload, per-GPU shape and
+    parallelism (KV-head shard: each rank holds Hkv / world KV heads and their query heads)."""
+    Hq, Hkv = wl["Hq"], wl["Hkv"]
+    if wl.get("kv_shard"):
+        Hq, Hkv = Hq // world, Hkv // world
+    cfg = dict(workload=wl["name"], requests_per_gpu=wl["R"], beam=wl["b"], prompt_len=wl["t"],
+               new_tokens=wl["s"], layers=wl["L"], q_heads_per_gpu=Hq, kv_heads_per_gpu=Hkv,
+               head_dim=wl["D"], vocab=wl["V"], window=wl["W"], gc_interval=wl.get("g", 1),
+               parallelism=(f"kv-head-shard{world} (per-layer all-gather of attention outputs)"
+                            if wl.get("kv_shard") else f"request-dp{world}"))
+    if wl.get("eos_frac"):
+        cfg["eos_frac"] = wl["eos_frac"]
+    return cfg
+
+
 # ------------------------------------------------------------------------------------------
 class HotPath:
     """Buffers, trie state and captured step graphs for one rank."""
@@ -562,13 +596,7 @@ def run_gpu(args):
         dist.barrier()
     _lib.load()
     dev = torch.device("cuda", local)
-    wl = dict(WORKLOADS[args.workload])
-    if args.beam:
-        wl["b"] = args.beam
-    if args.requests:
-        wl["R"] = args.requests
-    wl["g"] = args.gc_interval
-    wl["eos_frac"] = args.eos_frac
+    wl = _workload(args)
     if wl.get("kv_shard") and world > 1 and backend != "nccl":
         raise SystemExit("the KV-head shard's per-layer all-gather is captured in CUDA graphs: NCCL only")
     hp = HotPath(wl, rank, dev, world)
@@ -680,21 +708,14 @@ def run_gpu(args):
     units = R if hp.kv_shard else R * world
     value = units * args.steps / (ms * 1e-3)
     kv_fp = R * (t + s // 2) * hp.Hkv * hp.D * 4 * L
-    res = dict(metric="beam-decode steps/s (request-steps/s, hot path) + trie-attn HBM GB/s",
-               value=round(value, 2), unit="request-steps/s", n_gpus=world, steps=args.steps,
+    res = dict(metric=METRIC, value=round(value, 2), unit="request-steps/s", n_gpus=world, steps=args.steps,
                warmup=args.warmup, ms_per_step=round(ms / args.steps, 4), higher_is_better=True,
-               scaling="strong" if hp.kv_shard else "weak", vs_baseline=None, dtype="bf16", data="synthetic",
-               config=dict(workload=wl["name"], requests_per_gpu=R, beam=b, prompt_len=t,
-                           new_tokens=s, layers=L, q_heads_per_gpu=hp.Hq, kv_heads_per_gpu=hp.Hkv,
-                           head_dim=hp.D,
-                           vocab=hp.V, window=hp.W, gc_interval=hp.g,
-                           **({"eos_frac": wl["eos_frac"]} if wl.get("eos_frac") else {}),
-                           parallelism=(f"kv-head-shard{world} (per-layer all-gather of attention outputs)"
-                                        if hp.kv_shard else f"request-dp{world}"),
-                           execution="cuda-graph replay per step",
-                           attention={k: v for k, v in hp.plan["steady"].items()},
-                           l2=(f"no flush: each layer's pool is re-read once per step and the per-step "
-                               f"KV footprint ({kv_fp / 1e6:.0f} MB) > L2 (126 MB)")))
+               scaling=_scaling(wl), vs_baseline=None, dtype="bf16", data="synthetic",
+               config=bench_config(wl, world),
+               execution=dict(steps="cuda-graph replay per step",
+                              attention={k: v for k, v in hp.plan["steady"].items()},
+                              l2=(f"no flush: each layer's pool is re-read once per step and the per-step "
+                                  f"KV footprint ({kv_fp / 1e6:.0f} MB) > L2 (126 MB)")))
     res["roofline"] = dict(kernel="trie_attn_decode", bound="hbm", achieved=round(ach, 1), peak=peak,
                            unit="GB/s", frac=round(ach / peak, 4), frac_of_8TBps=round(ach / 8000, 4),
                            traffic=_traffic(args.workload, R, b), peak_source=peak_src,
@@ -830,79 +851,221 @@ def _traffic(workload, R, b):
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_oracle_sample(wl, budget_s=15.0, max_steps=64):
-    """Time the CPU oracle on a bounded sample of the workload: one request at a mid-job
-    trie state; one request-step = L x attn_ref (one layer) + beam_step_ref + GC.  The
-    oracle is timed as it stands (single BLAS thread)."""
-    from threadpoolctl import threadpool_limits
+# CPU oracle timing (the cpu_baseline leg and --impl reference): the oracle as it stands,
+# on the host cores of this box, over independent requests (the natural DP axis, SURVEY
+# §8(d)): one worker process per core, each one request, numpy fp64 with ONE BLAS thread.
+def cpu_info():
+    """nproc, usable cores, lscpu model and sockets of this host."""
+    info = {"nproc": os.cpu_count(), "usable_cores": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            if k.strip() == "Model name":
+                info["model"] = v.strip()
+            elif k.strip() == "Socket(s)":
+                info["sockets"] = v.strip()
+    except Exception:
+        pass
+    return info
 
+
+def _oracle_request(wl, req):
+    """One request of the workload at mid-job, built by the oracle itself: prompt (synth,
+    the bench's recipe), then k_mid = s/2 steps of the oracle's beam step over seeded
+    N(0, 3^2) logits (the bench's logit scale) with the trie update and GC of Alg. 2.
+    Q / K / V of the step are N(0, 1) (the bench's inputs); K / V [Hkv][N][D] stand for
+    one layer's pool, re-used by all L layers (each layer still runs attn_ref in full)."""
     import synth
-    from oracle.kernels_ref import attn_ref, beam_step_ref, build_tries
+    from oracle.kernels_ref import beam_step_ref
+    from oracle.trie import Trie, garbage_collect
+    t, b, V, s = wl["t"], wl["b"], wl["V"], wl["s"]
+    prompts, _ = synth.prompts(10_000 + req, 1, t, V)
+    T = Trie(prompts[0])
+    for k in range(s // 2):
+        lg = synth.normal(5_000 + req, k, (len(T.leaves), V)) * 3.0
+        par, tok, cs, _, _ = beam_step_ref(lg, T.scores, b)
+        T.update_trie([(float(c), int(v), int(j)) for c, v, j in zip(cs, tok, par)])
+        garbage_collect(T)
+    Hq, Hkv, D = wl["Hq"], wl["Hkv"], wl["D"]
+    return dict(T=T, q=synth.normal(6_000 + req, 1, (b, Hq, D)),
+                K=synth.normal(6_000 + req, 2, (Hkv, T.N, D)),
+                Vv=synth.normal(6_000 + req, 3, (Hkv, T.N, D)),
+                logits=synth.normal(6_000 + req, 4, (b, V)) * 3.0)
+
+
+def _oracle_request_step(st, wl):
+    """One request-step on the CPU oracle: L x attn_ref (a-3, every layer computed) +
+    beam_step_ref (a-4) + trie append (a-5) + GC mark / prune / compact (a-6) on a copy
+    (so every step starts from the same mid-job state)."""
+    import copy
+    from oracle.kernels_ref import attn_ref, beam_step_ref
     from oracle.trie import garbage_collect
-    L, Hq, Hkv, D, V, t, b, s = (wl[k] for k in ("L", "Hq", "Hkv", "D", "V", "t", "b", "s"))
-    prompts, lens = synth.prompts(1, 1, t, V)
-    k_mid = s // 2
-    sels = [(p[None], q[None]) for p, q in synth.selections(3, k_mid, b, V, 0.5)]
-    T = build_tries(prompts, lens, sels, b, g=1)[0]
-    N = T.N
-    q = synth.normal(4, 1, (b, Hq, D))
-    K = synth.normal(4, 2, (Hkv, N, D))
-    Vv = synth.normal(4, 3, (Hkv, N, D))
-    logits = synth.normal(4, 4, (b, V)) * 3.0
-    scores = np.zeros(b)
-    times = []
+    T = st["T"]
+    for _ in range(wl["L"]):
+        attn_ref(st["q"], st["K"], st["Vv"], T, window=wl["W"])
+    par, tok, cs, _, _ = beam_step_ref(st["logits"], T.scores, wl["b"])
+    Tc = copy.deepcopy(T)
+    Tc.update_trie([(float(c), int(v), int(j)) for c, v, j in zip(cs, tok, par)])
+    garbage_collect(Tc)
+
+
+def _oracle_worker(conn, wl, req):
+    from threadpoolctl import threadpool_limits
     with threadpool_limits(limits=1):
-        t_start = time.perf_counter()
-        while len(times) < max_steps:
-            a0 = time.perf_counter()
-            attn_ref(q, K, Vv, T, window=wl["W"])
-            a1 = time.perf_counter()
-            beam_step_ref(logits, scores, b)
-            a2 = time.perf_counter()
-            import copy
-            Tc = copy.deepcopy(T)
-            a3 = time.perf_counter()
-            garbage_collect(Tc)
-            a4 = time.perf_counter()
-            times.append(L * (a1 - a0) + (a2 - a1) + (a4 - a3))
-            if time.perf_counter() - t_start > budget_s:
-                break
-    return times, N
+        st = _oracle_request(wl, req)
+        conn.send(("ready", st["T"].N))
+        while conn.recv() is not None:
+            a = time.perf_counter()
+            _oracle_request_step(st, wl)
+            conn.send(time.perf_counter() - a)
 
 
-def cpu_baseline(wl, budget_s=15.0):
-    times, N = cpu_oracle_sample(wl, budget_s)
-    per = float(np.mean(times))
-    return {"value": round(1.0 / per, 4), "unit": "request-steps/s", "cores": 1, "kind": "oracle",
-            "sample": f"{len(times)} request-steps of one request at step {wl['s'] // 2} of its job "
-                      f"(N={N} trie rows): attn_ref timed on one layer and scaled x{wl['L']} layers, "
-                      f"+ beam_step_ref over b x V + GC (mark/prune/compact); numpy fp64, 1 BLAS thread"}
+def cpu_oracle_run(wl, steps, warmup, workers=None, budget_s=None):
+    """Time `steps` parallel request-steps (after `warmup`) of `workers` independent
+    requests (default: every usable core, at most 128), one process each, numpy with one
+    BLAS thread.  Returns (request-steps/s, dict of details).  Wall time per step is the
+    host clock around one request-step of every worker; `budget_s` stops early."""
+    import multiprocessing as mp
+    P = workers or min(len(os.sched_getaffinity(0)), 128)
+    env_keep = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for k in env_keep:
+        os.environ[k] = "1"
+    ctx = mp.get_context("spawn")
+    procs, conns = [], []
+    try:
+        for i in range(P):
+            a, c = ctx.Pipe()
+            p = ctx.Process(target=_oracle_worker, args=(c, wl, i), daemon=True)
+            p.start()
+            procs.append(p)
+            conns.append(a)
+        Ns = [c.recv()[1] for c in conns]
+        walls, per_req = [], []
+        t_start = None
+        for i in range(warmup + steps):
+            a = time.perf_counter()
+            for c in conns:
+                c.send(1)
+            dts = [c.recv() for c in conns]
+            w = time.perf_counter() - a
+            if i >= warmup:
+                if t_start is None:
+                    t_start = a
+                walls.append(w)
+                per_req.extend(dts)
+                if budget_s is not None and time.perf_counter() - t_start > budget_s:
+                    break
+        for c in conns:
+            c.send(None)
+    finally:
+        for p in procs:
+            p.join(timeout=5)
+            if p.is_alive():
+                p.terminate()
+        for k, v in env_keep.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    wall = float(np.sum(walls))
+    return P * len(walls) / wall, dict(
+        workers=P, steps=len(walls), wall_s=round(wall, 3), ms_per_step=round(wall / len(walls) * 1e3, 6),
+        per_request_step_s=round(float(np.mean(per_req)), 4), trie_rows_mean=round(float(np.mean(Ns)), 1))
+
+
+def _oracle_sample_text(wl, d):
+    return (f"{d['workers']} independent requests in parallel (one process per core, numpy fp64, "
+            f"1 BLAS thread each), {d['steps']} timed steps; each worker step = one request-step at "
+            f"step {wl['s'] // 2} of its job (oracle-built trie, {d['trie_rows_mean']} rows mean): "
+            f"attn_ref on all {wl['L']} layers (one layer's K/V re-used) + beam_step_ref over "
+            f"b x V + append + GC; host wall clock per step")
+
+
+def cpu_baseline(wl, budget_s=12.0):
+    v, d = cpu_oracle_run(wl, steps=64, warmup=1, budget_s=budget_s)
+    return {"value": round(v, 4), "unit": "request-steps/s", "cores": d["workers"], "kind": "oracle",
+            "sample": _oracle_sample_text(wl, d), "host": cpu_info(), **d}
 
 
 def run_reference(args):
+    """--impl reference: the CPU oracle as it stands on this box's host cores, on the GPU
+    arm's workload, metric, unit and config; K timed steps after W warm-up steps, each
+    step a request-step of every worker (rank 0 only; other ranks exit without work)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    wl = dict(WORKLOADS[args.workload])
-    if args.beam:
-        wl["b"] = args.beam
-    budget = 180.0
-    times, N = cpu_oracle_sample(wl, budget_s=budget, max_steps=args.warmup + args.steps)
-    timed = times[args.warmup:] or times
-    per = float(np.mean(timed))
-    v = 1.0 / per
-    res = dict(metric="beam-decode steps/s (request-steps/s, hot path) + trie-attn HBM GB/s",
-               value=round(v, 4), unit="request-steps/s", n_gpus=world, steps=len(timed),
-               warmup=args.warmup, ms_per_step=round(per * 1e3, 3), higher_is_better=True,
-               scaling="weak", vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
-               config=dict(workload=wl["name"], requests_per_gpu=1, beam=wl["b"], prompt_len=wl["t"],
-                           new_tokens=wl["s"], layers=wl["L"], parallelism="cpu-oracle"),
-               cpu_baseline=dict(value=round(v, 4), unit="request-steps/s", cores=1, kind="oracle",
-                                 sample=f"each step = one request-step of the CPU oracle (N={N} rows, "
-                                        f"attn_ref x{wl['L']} layers + beam_step_ref + GC)"),
+    wl = _workload(args)
+    v, d = cpu_oracle_run(wl, steps=args.steps, warmup=args.warmup)
+    res = dict(metric=METRIC, value=round(v, 4), unit="request-steps/s", n_gpus=world, steps=d["steps"],
+               warmup=args.warmup, ms_per_step=d["ms_per_step"], higher_is_better=True,
+               scaling=_scaling(wl), vs_baseline=None, dtype="f64", data="synthetic", impl="reference",
+               config=bench_config(wl, world),
+               cpu_baseline=dict(value=round(v, 4), unit="request-steps/s", cores=d["workers"], kind="oracle",
+                                 sample=_oracle_sample_text(wl, d), host=cpu_info(), **d),
                e2e=dict(value=round(v, 4), unit="request-steps/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     return res
+
+
+def run_oracle_units(args):
+    """--impl reference --units: SURVEY §8(d)'s per-unit CPU oracle timings on this host
+    (1 thread each): configs[0] full decodes (trie and batch, seconds), attn_ref per
+    (request, layer) at every bench shape, beam_step_ref at each V, GC."""
+    import copy
+
+    from threadpoolctl import threadpool_limits
+
+    import synth
+    from oracle.decode import batch_beam_search, trie_beam_search
+    from oracle.kernels_ref import attn_ref, beam_step_ref, build_tries
+    from oracle.model import Model, ModelConfig
+    from oracle.trie import garbage_collect
+    out = dict(kind="oracle per-unit timings, 1 thread", host=cpu_info(), units=[])
+
+    def timeit(fn, reps):
+        ts = []
+        for _ in range(reps):
+            a = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - a)
+        return float(np.median(ts))
+
+    with threadpool_limits(limits=1):
+        # configs[0]: tiny 2-layer MHA, prompt 8, b=3, 16 steps (fp64 oracle, seconds)
+        seed = 0
+        m = Model(synth.tiny_weights(seed, 2, 64, 4, 4, 16, 256, 256), ModelConfig())
+        prompts, _ = synth.prompts(seed, 1, 8, 256)
+        p0 = [int(x) for x in prompts[0]]
+        out["units"].append(dict(unit="configs[0] full decode, trie (Alg. 2)", seconds=round(
+            timeit(lambda: trie_beam_search(m, p0, 3, 16, g=1), 3), 4)))
+        out["units"].append(dict(unit="configs[0] full decode, batch (Alg. 1)", seconds=round(
+            timeit(lambda: batch_beam_search(m, p0, 3, 16), 3), 4)))
+        shapes = [("phi", {}), ("llama", {}), ("mistral-shard", {}), ("sweep", {"b": 16})]
+        for name, over in shapes:
+            wl = dict(WORKLOADS[name], **over)
+            t, b, V, s = wl["t"], wl["b"], wl["V"], wl["s"]
+            pr, ln = synth.prompts(1, 1, t, V)
+            T = build_tries(pr, ln, synth.selections(3, s // 2, b, V, 0.5), b, g=1)[0]
+            q = synth.normal(4, 1, (b, wl["Hq"], wl["D"]))
+            K = synth.normal(4, 2, (wl["Hkv"], T.N, wl["D"]))
+            Vv = synth.normal(4, 3, (wl["Hkv"], T.N, wl["D"]))
+            lg = synth.normal(4, 4, (b, V)) * 3.0
+            sc = np.zeros(b)
+            a = timeit(lambda: attn_ref(q, K, Vv, T, window=wl["W"]), 2)
+            bs = timeit(lambda: beam_step_ref(lg, sc, b), 2)
+            par, tok, cs, _, _ = beam_step_ref(lg, sc, b)
+
+            def gc_unit():
+                Tc = copy.deepcopy(T)
+                Tc.update_trie([(float(c), int(v), int(j)) for c, v, j in zip(cs, tok, par)])
+                garbage_collect(Tc)
+            gcs = timeit(gc_unit, 3)
+            out["units"].append(dict(
+                unit=f"{wl['name']} b={b}: request at step {s // 2} (dial rho=0.5, N={T.N})",
+                attn_ref_per_request_layer_s=round(a, 4), beam_step_ref_s=round(bs, 4),
+                append_gc_s=round(gcs, 5), request_step_all_layers_s=round(wl["L"] * a + bs + gcs, 3)))
+    return out
 
 
 def main():
@@ -921,11 +1084,13 @@ def main():
                     help="NEXT-3 experiment: EOS id 0 finishes this fraction of the requests early")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--units", action="store_true",
+                    help="with --impl reference: SURVEY 8(d) per-unit CPU oracle timings (1 thread)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
-        res = run_reference(args)
+        res = run_oracle_units(args) if args.units else run_reference(args)
         if res is not None:
             print(json.dumps(res))
         return
@@ -934,11 +1099,8 @@ def main():
         return
     res, ctx = run_gpu(args)
     if ctx["rank"] == 0:
-        wl = dict(WORKLOADS[args.workload])
-        if args.beam:
-            wl["b"] = args.beam
         if not args.no_cpu_baseline and ctx["world"] == 1:
-            res["cpu_baseline"] = cpu_baseline(wl)
+            res["cpu_baseline"] = cpu_baseline(_workload(args))
         print(json.dumps(res))
 
 

@@ -609,8 +609,8 @@ static const SkKernel* sk_select(int D) {
 static bool sk_env_enabled() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("TRIE_ATTN_STREAMK");
-    v = (e && e[0] == '0') ? 0 : 1;
+    const char* e = getenv("TRIE_ATTN_STREAMK");  // opt-in until it beats the per-item kernel
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }

@@ -53,3 +53,24 @@ def test_gc_schedule_matches_the_oracle(g):
     hp = types.SimpleNamespace(g=g, t=t)
     for k0 in range(s):
         assert bench.HotPath.gc_now(hp, k0) == ((t + (k0 + 1)) % g == 0)
+
+
+def test_reference_arm_shares_the_gpu_arm_config():
+    """--impl reference reports the GPU arm's exact `config` (same workload, shape, parallelism)."""
+    args = types.SimpleNamespace(workload="phi", beam=0, requests=0, gc_interval=1, eos_frac=0.0)
+    wl = bench._workload(args)
+    cfg = bench.bench_config(wl, 1)
+    assert cfg["workload"] == bench.WORKLOADS["phi"]["name"] and cfg["requests_per_gpu"] == 64
+    assert cfg["parallelism"] == "request-dp1"
+    shard = bench.bench_config(dict(bench.WORKLOADS["mistral-shard"], g=1), 8)
+    assert shard["kv_heads_per_gpu"] == 1 and shard["q_heads_per_gpu"] == 4
+
+
+def test_cpu_oracle_run_is_measured_per_step():
+    """The CPU oracle leg times every layer for real: 2 worker processes, a tiny workload,
+    and a wall clock per step that covers L x attn_ref (no extrapolation)."""
+    wl = dict(name="tiny", L=2, Hq=4, Hkv=2, D=16, V=64, t=20, b=3, s=6, R=2, W=0)
+    v, d = bench.cpu_oracle_run(wl, steps=3, warmup=1, workers=2)
+    assert d["workers"] == 2 and d["steps"] == 3 and v > 0
+    assert abs(v - 2 * 3 / (d["ms_per_step"] * 3e-3)) <= 1e-2 * v
+    assert d["per_request_step_s"] * 1e3 <= d["ms_per_step"] * 1.5
