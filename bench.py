@@ -154,6 +154,16 @@ def bench_config(wl, world):
     return cfg
 
 
+class _Eager:
+    """Stand-in for a captured graph in the eager test mode: replay() re-runs the ops."""
+
+    def __init__(self, fn):
+        self.fn = fn
+
+    def replay(self):
+        self.fn()
+
+
 # ------------------------------------------------------------------------------------------
 class HotPath:
     """Buffers, trie state and captured step graphs for one rank."""
@@ -169,6 +179,10 @@ class HotPath:
         L, Hq, Hkv, D, V, t, b, s, R, W = (wl[k] for k in ("L", "Hq", "Hkv", "D", "V", "t", "b", "s", "R", "W"))
         self.kv_shard = bool(wl.get("kv_shard"))
         self.world = world
+        # eager test mode (BENCH_DIST_BACKEND=gloo, several ranks per GPU): the KV-head
+        # shard's per-layer all-gather cannot be captured in a graph over gloo, so steps
+        # run eagerly and the gather goes through host memory; the driver's runs are NCCL
+        self.eager = self.kv_shard and world > 1 and os.environ.get("BENCH_DIST_BACKEND", "nccl") != "nccl"
         if self.kv_shard:  # this rank's KV heads and their query heads
             _, Hkv, _, Hq = tdist.kv_head_shard(Hq, Hkv, world, rank)
         self.L, self.Hq, self.Hkv, self.D, self.V, self.t, self.b, self.s, self.R, self.W = \
@@ -281,7 +295,11 @@ class HotPath:
     def _gather(self, out):
         from paper_2502_00085_b200.dist import gather_heads
         # the first step of a job has one live beam: its own buffer
-        gather_heads(out, self.gathered if out.shape[1] == self.b else self.gathered1)
+        dst = self.gathered if out.shape[1] == self.b else self.gathered1
+        if self.eager:  # gloo: through host memory
+            dst.copy_(gather_heads(out.cpu()))
+            return
+        gather_heads(out, dst)
 
     def capture(self):
         """One graph per (variant, slot) + an event-instrumented twin for kernel timing."""
@@ -299,11 +317,18 @@ class HotPath:
                             evs = [(torch.cuda.Event(enable_timing=True, external=True),
                                     torch.cuda.Event(enable_timing=True, external=True))
                                    for _ in range(n_pairs)]
+                        key = ((var, gc), slot, timed)
+                        if self.eager:
+                            self.graphs[key] = _Eager(
+                                lambda var=var, slot=slot, evs=evs, gc=gc: self.step_ops(var, slot, evs, gc))
+                            self.launches_per_graph[key] = None  # counted at run time
+                            if timed:
+                                self.ev[((var, gc), slot)] = evs
+                            continue
                         g = torch.cuda.CUDAGraph()
                         n0 = _lib.trie_launch_count()
                         with torch.cuda.graph(g):
                             self.step_ops(var, slot, evs, gc)
-                        key = ((var, gc), slot, timed)
                         self.graphs[key] = g
                         self.launches_per_graph[key] = _lib.trie_launch_count() - n0
                         if timed:
@@ -319,6 +344,17 @@ class HotPath:
         torch = self.torch
         st, L = self.st, self.L
         d = self.inp[("steady", 0)]
+        if self.eager:  # the host view is still at its warm-up state: b live beams after step 1
+            def attn_only():
+                for l in range(L):
+                    q, k, v = d["views"][l]
+                    if self.fused["steady"]:
+                        st.attn_decode_rope(q, k, v, self.kp[l], self.vp[l], self.wl["theta"], d["out"],
+                                            rows_hint=self.rows_hint)
+                    else:
+                        st.attn_decode(q, self.kp[l], self.vp[l], d["out"], rows_hint=self.rows_hint)
+            self.attn_graph = _Eager(attn_only)
+            return
         assert st.b_live == self.b, "attention-only graph must be captured with b live beams"
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
@@ -597,8 +633,6 @@ def run_gpu(args):
     _lib.load()
     dev = torch.device("cuda", local)
     wl = _workload(args)
-    if wl.get("kv_shard") and world > 1 and backend != "nccl":
-        raise SystemExit("the KV-head shard's per-layer all-gather is captured in CUDA graphs: NCCL only")
     hp = HotPath(wl, rank, dev, world)
     R, L, s, b, t = hp.R, hp.L, hp.s, hp.b, hp.t
 
@@ -649,11 +683,15 @@ def run_gpu(args):
 
     # Region A (value): plain step graphs back to back.
     t0.record(stream)
+    n_launch0 = _lib.trie_launch_count()  # eager mode: host-side launch counter
     for i in range(args.steps):
         k_hist.append(hp.k)
         n_hist[i].copy_(hp.st.n_nodes, non_blocking=True)  # 4*R bytes, for byte accounting
         var = hp.replay(i % 2)
-        launches += hp.launches_per_graph[(var, i % 2, False)]
+        if not hp.eager:
+            launches += hp.launches_per_graph[(var, i % 2, False)]
+    if hp.eager:
+        launches = _lib.trie_launch_count() - n_launch0
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
@@ -712,7 +750,8 @@ def run_gpu(args):
                warmup=args.warmup, ms_per_step=round(ms / args.steps, 4), higher_is_better=True,
                scaling=_scaling(wl), vs_baseline=None, dtype="bf16", data="synthetic",
                config=bench_config(wl, world),
-               execution=dict(steps="cuda-graph replay per step",
+               execution=dict(steps=("eager (gloo test mode: host-memory all-gather)" if hp.eager
+                                     else "cuda-graph replay per step"),
                               attention={k: v for k, v in hp.plan["steady"].items()},
                               l2=(f"no flush: each layer's pool is re-read once per step and the per-step "
                                   f"KV footprint ({kv_fp / 1e6:.0f} MB) > L2 (126 MB)")))
@@ -1046,7 +1085,8 @@ def run_oracle_units(args):
             wl = dict(WORKLOADS[name], **over)
             t, b, V, s = wl["t"], wl["b"], wl["V"], wl["s"]
             pr, ln = synth.prompts(1, 1, t, V)
-            T = build_tries(pr, ln, synth.selections(3, s // 2, b, V, 0.5), b, g=1)[0]
+            sels = [(p_[None], q_[None]) for p_, q_ in synth.selections(3, s // 2, b, V, 0.5)]
+            T = build_tries(pr, ln, sels, b, g=1)[0]
             q = synth.normal(4, 1, (b, wl["Hq"], wl["D"]))
             K = synth.normal(4, 2, (wl["Hkv"], T.N, wl["D"]))
             Vv = synth.normal(4, 3, (wl["Hkv"], T.N, wl["D"]))

@@ -679,6 +679,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
   }
   if constexpr (RS > 1) {
     // row-slice merge: slices rs > 0 park (O, m, l) in the drained ring, slice 0 folds them
+    __syncwarp();
     asm volatile("bar.sync 1, %0;" ::"r"(C::NC * 32));
     float* red = (float*)smem;  // [(RS-1) * MT][16][D + 2]
     constexpr int RW = D + 2;
@@ -699,6 +700,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
         mine[(gq + 8) * RW + D + 1] = lrow[1];
       }
     }
+    __syncwarp();
     asm volatile("bar.sync 1, %0;" ::"r"(C::NC * 32));
     if (rs > 0) return;
 #pragma unroll

@@ -38,7 +38,8 @@
 
 namespace trie {
 
-constexpr int SK_MAX_R = 256;  // requests per launch held in the shared-memory table
+constexpr int SK_MAX_R = 256;
+constexpr bool ROPE_PF = true;  // L2-prefetch the RoPE table rows of later segments too  // requests per launch held in the shared-memory table
 
 template <int D, int MT, int RS, int ST>
 struct SkCfg {
@@ -175,7 +176,7 @@ __device__ __forceinline__ void sk_table(const AttnParams& p, int4* rq, int* ff,
 }
 
 template <int D, int MT, int RS, int ST>
-__global__ void __launch_bounds__(SkCfg<D, MT, RS, ST>::THREADS, 2) k_attn_wide_sk(
+__global__ void __maxnreg__(200) k_attn_wide_sk(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p, const __grid_constant__ CUtensorMap kmh,
     const __grid_constant__ CUtensorMap vmh) {
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(SkCfg<D, MT, RS, ST>::THREADS, 2) k_attn_wide_
 
   pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x, c = blockIdx.x;
+  const int c = blockIdx.x;
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
@@ -209,6 +210,10 @@ __global__ void __launch_bounds__(SkCfg<D, MT, RS, ST>::THREADS, 2) k_attn_wide_
     __threadfence_block();
     asm volatile("bar.arrive 2, %0;" ::"r"(C::THREADS) : "memory");
     const int W = pre[p.R];
+    // G = min(grid, W): every CTA range non-empty, so an item's participants are exactly
+    // the CTAs cf..cl its tiles map to (the merge ticket counts them)
+    const int G = min((int)gridDim.x, W);
+    if (c >= G) return;
     SkIter it{rq, pre, p.R, p.Hkv};
     it.start(sk_bound(c, W, G), sk_bound(c + 1, W, G));
     if (lane != 0) {
@@ -279,9 +284,34 @@ __global__ void __launch_bounds__(SkCfg<D, MT, RS, ST>::THREADS, 2) k_attn_wide_
   }
   asm volatile("bar.sync 2, %0;" ::"r"(C::THREADS) : "memory");  // the table is published
   const int W = pre[p.R];
+  const int G = min((int)gridDim.x, W);
+  if (c >= G) return;
   SkIter it{rq, pre, p.R, p.Hkv};
   const int b0 = sk_bound(c, W, G);
   it.start(b0, sk_bound(c + 1, W, G));
+  {
+    // the Q rows and RoPE table of the CTA's later segments: into L2 now, so a segment
+    // switch does not wait a loaded-HBM round trip (the first segment's are read at once)
+    SkIter pf = it;
+    SkSeg s;
+    bool first = true;
+    while (pf.next(s)) {
+      if (first) { first = false; continue; }
+      const int m = mt * 16 + (lane >> 1);
+      if (m < Qg) {
+        const int j = m / g;
+        const char* qa = (const char*)((const __nv_bfloat16*)p.q +
+                                       (((size_t)s.r * p.b_live + j) * p.Hq + s.h * g + m - j * g) * D);
+        for (int off = (lane & 1) * 128; off < D * 2; off += 256)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(qa + off));
+        if (ROPE_PF && rs == 0 && (m % g) == 0) {
+          const char* rt = (const char*)(p.rope_tab + ((size_t)s.r * p.b_live + j) * (D / 2));
+          for (int off = (lane & 1) * 128; off < D * 4; off += 256)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rt + off));
+        }
+      }
+    }
+  }
   int gi = 0;
   SkSeg s;
   while (it.next(s)) {
@@ -444,6 +474,7 @@ __global__ void __launch_bounds__(SkCfg<D, MT, RS, ST>::THREADS, 2) k_attn_wide_
       // slices rs > 0 park (O, m, l) in the held stage, slice 0 folds them in
       constexpr int RW = D + 2;
       float* red = (float*)(ring + st_last * RG::STAGE_BYTES);
+      __syncwarp();
       asm volatile("bar.sync 1, %0;" ::"r"(C::NC * 32) : "memory");  // the stage's K/V are consumed
       if (rs > 0) {
         float* mine = red + (size_t)((rs - 1) * MT + mt) * 16 * RW;
@@ -458,6 +489,7 @@ __global__ void __launch_bounds__(SkCfg<D, MT, RS, ST>::THREADS, 2) k_attn_wide_
           *(float2*)&mine[(gq + 8) * RW + D] = make_float2(mrow[1], lrow[1]);
         }
       }
+      __syncwarp();
       asm volatile("bar.sync 1, %0;" ::"r"(C::NC * 32) : "memory");
       if (rs == 0) {
 #pragma unroll

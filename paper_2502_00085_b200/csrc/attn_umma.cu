@@ -224,7 +224,6 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
   uint32_t* trc = nullptr;
 #define TRC(i, k) do { } while (0)
 #endif
-  constexpr int QBAR_THREADS = (C::NSW + 1) * 32;
 
   if (warp == 0 || warp == 3 + C::NSW) {
     // ============ TMA producers: warp 0 = K tiles, the last warp = V tiles + mask words ============
@@ -271,7 +270,7 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
     const uint32_t idesc_qk = umma_idesc(128, 64, 0);
     const uint32_t idesc_pv = umma_idesc(128, D, 1);
     if (warp == 2) {
-      asm volatile("bar.sync 1, %0;" ::"r"(QBAR_THREADS));  // Q staged by the softmax warps
+      mbar_wait(app_done, 0u);  // Q staged (and the leaf rows appended) by the softmax warps
       tc_fence_after();
       const uint32_t qbase = smem_u32(qsm);
       for (int i = 0; i < ntiles; ++i) {
@@ -378,8 +377,11 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
         append_leaves_rope_work<D>(p, r, h, it.tile0 * TC_TR, (it.tile0 + ntiles) * TC_TR, tid,
                                    C::NSW * 32, it.N - p.b_live);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 1, %0;" ::"r"(QBAR_THREADS));
-      if (ROPE && tid == 0) mbar_arrive(app_done);  // every softmax thread's append is fenced
+      // softmax warps only (one call site); then one arrival publishes Q (and, fused,
+      // every softmax thread's fenced append) to the QK issuer and the producers
+      __syncwarp();
+      asm volatile("bar.sync 1, %0;" ::"r"(C::NSW * 32));
+      if (tid == 0) mbar_arrive(app_done);
     }
     if (sp < n_live) {  // warps of padding-only sub-partitions have nothing to do
       const bool qvalid = row < Qg;
@@ -499,6 +501,7 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
       }
       float2* xb = xch + sp * 64;
       xb[grp * 32 + lane] = make_float2(m_run, l_run);
+      __syncwarp();
       asm volatile("bar.sync %0, 64;" ::"r"(2 + sp));
       const float2 ot = xb[(1 - grp) * 32 + lane];
       // the other group's last PV must be complete too before O_{1-grp} is read

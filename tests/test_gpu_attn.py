@@ -343,7 +343,9 @@ def test_leaf_latch_and_reset_clears_status():
     st.beam_step(torch.randn(1, 1, 50, device="cuda"))
     assert st.status() == 0
     st.leaf[0, 1] = 9999
-    st.beam_step(torch.randn(1, 3, 50, device="cuda"))
+    lg = torch.randn(1, 3, 50, device="cuda")
+    lg[0, 1] += 100.0  # every new beam's parent is the corrupted beam 1
+    st.beam_step(lg)
     assert st.status() & _lib.TRIE_ST_LEAF
     st.reset()
     assert st.status() == 0
