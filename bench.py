@@ -129,6 +129,14 @@ def _workload(args):
         wl["b"] = args.beam
     if args.requests:
         wl["R"] = args.requests
+    if getattr(args, "prompt_len", 0):
+        wl["t"] = args.prompt_len
+        wl["name"] += f"-t{args.prompt_len}"
+    if getattr(args, "new_tokens", 0):
+        wl["s"] = args.new_tokens
+        wl["name"] += f"-s{args.new_tokens}"
+    if getattr(args, "logit_scale", 0.0):
+        wl["kappa"] = args.logit_scale
     wl["g"] = args.gc_interval
     wl["eos_frac"] = args.eos_frac
     return wl
@@ -151,6 +159,8 @@ def bench_config(wl, world):
                             if wl.get("kv_shard") else f"request-dp{world}"))
     if wl.get("eos_frac"):
         cfg["eos_frac"] = wl["eos_frac"]
+    if "kappa" in wl:
+        cfg["logit_scale"] = wl["kappa"]
     return cfg
 
 
@@ -211,7 +221,7 @@ class HotPath:
             per_layer = R * bl * (Hq + 2 * Hkv) * D
             for slot in range(self.NB):
                 qkv = torch.randn(L * per_layer, device=dev, generator=gen).to(torch.bfloat16)
-                lg = torch.randn(R * bl * V, device=dev, generator=lgen) * 3.0
+                lg = torch.randn(R * bl * V, device=dev, generator=lgen) * float(wl.get("kappa", 3.0))
                 if wl.get("eos_frac", 0.0) > 0.0 and var == "steady":
                     # NEXT-3 experiment (--eos-frac f): EOS (token 0) is the argmax of every
                     # row of the first round(f R) requests, so they finish at their second
@@ -646,6 +656,15 @@ def run_gpu(args):
     hp.k = 0
     for i in range(args.warmup):
         hp.replay(i % 2)
+    # untimed positioning replays: the K timed steps cover the MIDDLE of a job (job steps
+    # k0 .. k0+K-1 with k0 = (s - K) / 2) so a short run is not biased to the small tries
+    # of a job's start; K >= s covers whole jobs from wherever the warm-up left off
+    n_pos = 0
+    if args.steps < s:
+        k0 = (s - args.steps) // 2
+        while hp.k != k0:
+            hp.replay((args.warmup + n_pos) % 2)
+            n_pos += 1
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -699,10 +718,25 @@ def run_gpu(args):
         tt = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    # Region B (roofline): the same K steps continued with the instrumented graphs (event
-    # nodes around every attention launch; event-record nodes add ~5 us of graph latency
-    # each, so they are kept out of region A).  Slot i%2's events are harvested just
-    # before that slot is replayed again, waiting only for that step's end event.
+    def advance_to(kt):  # untimed plain replays up to job step kt (the next job's if passed)
+        while hp.k != kt:
+            hp.replay(0)
+    kA = k_hist[0] if args.steps < s else None
+    # Region C (roofline): the L attention launches of one step (steady beams) as one graph
+    # of back-to-back launches, replayed between CUDA events on the launching stream --
+    # kernel time without the event-node latency that region B's per-launch events add --
+    # on the trie at the MIDDLE of region A's window (same job step, next job)
+    if kA is not None:
+        advance_to((kA + args.steps // 2) % s)
+    c_us, c_bytes = hp.attn_only_timing(reps=max(4, min(20, 2 * args.steps)))
+    k_c = hp.k
+    # Region B (roofline): region A's window again (same job steps, next job) with the
+    # instrumented graphs (event nodes around every attention launch; event-record nodes
+    # add ~5 us of graph latency each, so they are kept out of region A).  Slot i%2's
+    # events are harvested just before that slot is replayed again, waiting only for that
+    # step's end event.
+    if kA is not None:
+        advance_to(kA)
     n_hist_b = torch.empty(args.steps, R, dtype=torch.int32, device=dev)
     t2 = torch.cuda.Event(enable_timing=True)
     t3 = torch.cuda.Event(enable_timing=True)
@@ -732,11 +766,6 @@ def run_gpu(args):
     st_bits = hp.st.status()
     assert st_bits == 0, f"device status bits {st_bits:#x}"
     in_step_gbs = float(np.sum(attn_bytes) / (np.sum(attn_ms) * 1e-3) / 1e9)
-    # Region C (roofline): the L attention launches of the current step (steady beams, the
-    # trie as the timed steps left it) as one graph of back-to-back launches, replayed
-    # between CUDA events on the launching stream -- kernel time without the event-node
-    # latency that region B's per-launch events add
-    c_us, c_bytes = hp.attn_only_timing(reps=max(4, min(20, 2 * args.steps)))
     # clocks sampled across regions A, B and C (contiguous GPU work, 100 ms period)
     clk = clocks.stop()
     ach = c_bytes / (c_us * 1e-6) / 1e9
@@ -763,8 +792,9 @@ def run_gpu(args):
                            kernel_launch=("trie_attn_decode_rope (fused a-1 + a-3; bytes counted: a-3 only)"
                                           if hp.fused["steady"] else "trie_attn_decode"),
                            timing=(f"CUDA events around a graph of the step's {hp.L} attention launches "
-                                   f"(one per layer, back to back, at step {hp.k} of a job), replayed "
-                                   f"after the timed steps; achieved = algorithmic bytes / mean launch time"),
+                                   f"(one per layer, back to back, at step {k_c} of a job: the middle of "
+                                   f"the timed window), replayed after the timed steps; achieved = "
+                                   f"algorithmic bytes / mean launch time"),
                            in_step=dict(achieved=round(in_step_gbs, 1),
                                         avg_launch_us=round(float(np.mean(attn_ms)) * 1e3, 2),
                                         attn_share_of_step=round(float(np.sum(attn_ms)) / ms_b, 4),
@@ -800,12 +830,55 @@ def run_gpu(args):
                                                  for i in range(len(k_hist))],
                                         batch_MB=[round(R * (b if k > 0 else 1) * (t + k) * kv_row / 1e6, 1)
                                                   for k in k_hist]))
+    res["execution"]["timed_job_steps"] = [int(k_hist[0]), int(k_hist[-1])]
+    if args.series:
+        res["series"] = run_series(hp, advance_to)
     if not args.no_e2e:
         res["e2e"] = run_e2e(hp, args, world)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return res, dict(rank=rank, world=world)
+
+
+def run_series(hp, advance_to):
+    """--series: one whole job (s steps from k = 0) replayed with the instrumented graphs,
+    synchronised per step: per-step attention (all L layers), beam-step and GC times
+    (CUDA event nodes), the trie rows before each step (summed over requests) and batch
+    beam search's b (t + k) rows -- the Fig. 4 (GC vs decoding pass) and
+    tab:ablation (saved KV entries) experiments."""
+    torch = hp.torch
+    advance_to(0)
+    torch.cuda.synchronize()
+    out = dict(k=[], attn_ms=[], beam_ms=[], gc_ms=[], gc_ran=[], trie_rows=[], batch_rows=[])
+    for i in range(hp.s):
+        k = hp.k
+        rows = int(hp.st.n_nodes.sum().item()) if k > 0 else hp.R * hp.t
+        key = hp.next_key()
+        hp.replay(i % 2, timed=True)
+        torch.cuda.synchronize()
+        evs = hp.ev[(key, i % 2)]
+        out["k"].append(k)
+        out["attn_ms"].append(round(sum(e0.elapsed_time(e1) for e0, e1 in evs[:-2]), 4))
+        out["beam_ms"].append(round(evs[-2][0].elapsed_time(evs[-2][1]), 4))
+        out["gc_ms"].append(round(evs[-1][0].elapsed_time(evs[-1][1]) if key[1] else 0.0, 4))
+        out["gc_ran"].append(bool(key[1]))
+        out["trie_rows"].append(rows)
+        out["batch_rows"].append(hp.R * (hp.b if k > 0 else 1) * (hp.t + k))
+    tr, br = np.array(out["trie_rows"], float), np.array(out["batch_rows"], float)
+    gc = np.array(out["gc_ms"])[np.array(out["gc_ran"])]
+    pas = np.array(out["attn_ms"]) + np.array(out["beam_ms"])
+    out["summary"] = dict(
+        requests=hp.R, gc_interval=hp.g,
+        saved_rows_per_request_mean=round(float((br - tr).mean()) / hp.R, 1),
+        saved_rows_per_request_final=round(float(br[-1] - tr[-1]) / hp.R, 1),
+        trie_over_batch_rows_mean=round(float((tr / br).mean()), 4),
+        gc_ms_mean=round(float(gc.mean()), 4) if len(gc) else None,
+        pass_ms_mean=round(float(pas.mean()), 4),
+        gc_over_pass_max=round(float((np.array(out["gc_ms"]) / pas).max()), 4),
+        note="rows = KV entries (one per token per layer set); trie rows before each step, "
+             "batch = b (t + k) per request (prompt replicated, P:42 counting)")
+    return out
 
 
 def run_e2e(hp, args, world):
@@ -1124,6 +1197,12 @@ def main():
                     help="NEXT-3 experiment: EOS id 0 finishes this fraction of the requests early")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--series", action="store_true",
+                    help="NEXT-1 experiments: one whole instrumented job, per-step times and rows")
+    ap.add_argument("--prompt-len", type=int, default=0)
+    ap.add_argument("--new-tokens", type=int, default=0)
+    ap.add_argument("--logit-scale", type=float, default=0.0,
+                    help="scale of the synthetic N(0, 1) logits (the convergence knob kappa; default 3)")
     ap.add_argument("--units", action="store_true",
                     help="with --impl reference: SURVEY 8(d) per-unit CPU oracle timings (1 thread)")
     args = ap.parse_args()

@@ -176,7 +176,7 @@ __device__ __forceinline__ void sk_table(const AttnParams& p, int4* rq, int* ff,
 }
 
 template <int D, int MT, int RS, int ST>
-__global__ void __maxnreg__(200) k_attn_wide_sk(
+__global__ void __launch_bounds__(SkCfg<D, MT, RS, ST>::THREADS, 2) k_attn_wide_sk(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p, const __grid_constant__ CUtensorMap kmh,
     const __grid_constant__ CUtensorMap vmh) {
