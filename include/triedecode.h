@@ -159,8 +159,7 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
 
 /*
  * Which attention kernel a configuration uses (host only): info_host[0] = path (0 CUDA-core
- * fp32/other, 1 narrow mma.sync, 2 wide mma.sync, 3 tcgen05/TMEM, 4 wide mma.sync with the
- * stream-K split of trie_attn_decode_rope),
+ * fp32/other, 1 narrow mma.sync, 2 wide mma.sync, 3 tcgen05/TMEM),
  * [1] = split-K count, [2] = 1 if trie_attn_decode_rope fuses into one launch, [3] = Qg.
  */
 int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,

@@ -232,7 +232,7 @@ def trie_launch_count() -> int:
     return int(load().trie_launch_count())
 
 
-ATTN_PATHS = {0: "cuda-core", 1: "narrow-mma.sync", 2: "wide-mma.sync", 3: "tcgen05-tmem", 4: "wide-streamk"}
+ATTN_PATHS = {0: "cuda-core", 1: "narrow-mma.sync", 2: "wide-mma.sync", 3: "tcgen05-tmem"}
 
 
 def trie_attn_plan_info(cfg: trie_cfg, b_live: int, rows_hint: int = 0) -> dict:

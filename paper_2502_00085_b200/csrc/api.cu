@@ -111,7 +111,6 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
   char* ss = take(R * b * 4);
   char* rtab = take(R * TRIE_MAX_BEAMS * (c->head_dim / 2) * 8);
   char* fin = take(R * TRIE_MAX_BEAMS * 4);
-  char* atk = take(R * c->n_kv_heads * 8 * 4);
   if (h) {
     h->token = (int32_t*)token;
     h->parent = (int32_t*)parent;
@@ -140,7 +139,6 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
     h->sel_score = (float*)ss;
     h->rope_tab = (float2*)rtab;
     h->fin = (uint32_t*)fin;
-    h->attn_tickets = (uint32_t*)atk;
     h->chunks = (int32_t)chunks;
   }
   return off;
@@ -196,8 +194,6 @@ int trie_create(const trie_cfg* cfg, void* workspace, size_t workspace_bytes,
   if (e == cudaSuccess) e = cudaMemsetAsync(h->status, 0, 4, stream);
   if (e == cudaSuccess)
     e = cudaMemsetAsync(h->cnt_row, 0, (size_t)cfg->n_requests * (TRIE_MAX_BEAMS + 1) * 4, stream);
-  if (e == cudaSuccess)
-    e = cudaMemsetAsync(h->attn_tickets, 0, (size_t)cfg->n_requests * cfg->n_kv_heads * 8 * 4, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // prompt_lens_host may be freed
   if (e != cudaSuccess) {
     delete h;
@@ -295,7 +291,6 @@ static size_t part_bytes(const trie_cfg* c, int b_live, int splits) {
 // everywhere and is kept only as profiles/r08_experiments/attn_persist.patch.)
 struct AttnPlan {
   int splits;
-  int sk_grid;  // > 0: the stream-K wide kernel with this many CTAs (fused path)
   size_t counter_bytes, part_bytes, mask_bytes;
 };
 
@@ -307,11 +302,6 @@ static AttnPlan attn_plan(const trie_cfg* c, int b_live, int rows_hint, bool rop
   sp.rows_hint = rows;
   pl.splits = trie::attn_plan_splits(sp, rows, sm_count());
   pl.part_bytes = align_up(part_bytes(c, b_live, pl.splits));
-  if (rope && trie::attn_sk_eligible(sp)) {
-    pl.splits = 1;
-    pl.sk_grid = trie::attn_sk_grid(sp, sm_count());
-    pl.part_bytes = align_up(trie::attn_sk_part_bytes(sp, sm_count()));
-  }
   pl.mask_bytes = align_up((size_t)c->n_requests * c->capacity * 4);
   return pl;
 }
@@ -389,7 +379,6 @@ int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,
     path = trie::attn_umma_eligible(p) ? 3 : (Qg <= 16 ? 1 : 2);
   p.k = p.v = (const void*)(uintptr_t)256;  // aligned placeholders for the shape test
   const bool fused = trie::attn_rope_fusable(p);
-  if (fused && path == 2 && attn_plan(cfg, b_live, rows_hint, true).sk_grid > 0) path = 4;
   info_host[0] = path;
   info_host[1] = fused ? attn_plan(cfg, b_live, rows_hint, true).splits : pl.splits;
   info_host[2] = fused ? 1 : 0;
@@ -450,11 +439,6 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.aux = scratch;
   p.part = (float*)((char*)scratch + pl.counter_bytes);
   p.splits = pl.splits;
-  if (pl.sk_grid > 0) {  // stream-K wide kernel (attn_streamk.cu)
-    if (h->eos >= 0) p.fin = h->fin;
-    p.tickets = h->attn_tickets;
-    return trie::launch_attn_wide_sk(p, pl.sk_grid, stream);
-  }
   // NEXT-3: with an EOS id, the fused kernels skip requests whose beams all finished
   if (h->eos >= 0) p.fin = h->fin;
   if (cfg->window == 0 && prefetch_enabled()) {

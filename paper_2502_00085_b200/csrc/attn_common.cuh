@@ -39,9 +39,6 @@ struct AttnParams {
   // NEXT-3 (narrow / wide, handle path with an EOS id): fin [R][32] finished flags; a
   // request whose b_live beams are all finished is done -- its CTAs read and write nothing
   const uint32_t* fin;
-  // stream-K wide path (attn_streamk.cu, handle path): per-(request, KV head, m-tile)
-  // merge tickets in the handle's workspace, zero between launches
-  uint32_t* tickets;
 };
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);
@@ -54,9 +51,5 @@ bool attn_tc_shape_ok(const AttnParams& p);
 bool attn_umma_eligible(const AttnParams& p);
 int attn_umma_occ(const AttnParams& p);
 int launch_attn_umma(const AttnParams& p, cudaStream_t s);
-bool attn_sk_eligible(const AttnParams& p);
-int attn_sk_grid(const AttnParams& p, int sms);
-size_t attn_sk_part_bytes(const AttnParams& p, int sms);
-int launch_attn_wide_sk(const AttnParams& p, int grid, cudaStream_t s);
 
 }  // namespace trie

@@ -41,7 +41,6 @@ struct trie_handle {
   float* sel_score = nullptr;     // [R][b]
   float2* rope_tab = nullptr;     // [R][b_live][D/2] (cos, sin) at the leaves' depths
   uint32_t* fin = nullptr;        // [R][32] beam finished (its last token is eos; NEXT-3)
-  uint32_t* attn_tickets = nullptr;  // [R][Hkv][8] stream-K merge tickets (zeroed at create)
   int32_t eos = -1;               // trie_set_eos; -1 = no EOS (the hot path)
   int32_t rope_tab_steps = -1;    // host: step count the table was computed for
   float rope_tab_theta = 0.f;

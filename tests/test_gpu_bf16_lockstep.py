@@ -1,5 +1,5 @@
 """Model-driven bf16 lockstep decode: the production bf16 kernels (fused RoPE + append +
-trie attention -- narrow / wide / tcgen05, and the stream-K wide path where planned --,
+trie attention -- narrow / wide / tcgen05 --
 the beam step and GC) run for >= 16 steps inside a random-init decoder, and after every
 step every layer is checked against the oracle on the SAME inputs (SURVEY §8(c)
 "snapshot-differential" checks; the lockstep protocol: the oracle follows the GPU's own
@@ -33,8 +33,8 @@ pytestmark = pytest.mark.gpu
 CASES = [
     ("narrow-mha", 64, 4, 4, 4, 3, 150, 18, 0, ("narrow-mma.sync",)),
     ("narrow-gqa", 64, 8, 2, 4, 3, 140, 17, 0, ("narrow-mma.sync",)),
-    ("wide", 128, 8, 2, 8, 3, 150, 17, 0, ("wide-mma.sync", "wide-streamk")),
-    ("wide-swa", 128, 8, 2, 8, 2, 130, 17, 100, ("wide-mma.sync", "wide-streamk")),
+    ("wide", 128, 8, 2, 8, 3, 150, 17, 0, ("wide-mma.sync",)),
+    ("wide-swa", 128, 8, 2, 8, 2, 130, 17, 100, ("wide-mma.sync",)),
     ("tcgen05", 128, 8, 1, 8, 2, 150, 17, 0, ("tcgen05-tmem",)),
 ]
 
