@@ -36,16 +36,16 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     # BASELINE.json configs[1]: the N=1 metric workload
-    "phi": dict(name="phi3.5-mini-mha-cnndm-t800-b4-s64", L=32, Hq=32, Hkv=32, D=96, V=32064,
+    "phi": dict(name="phi3.5-mini-mha-cnndm-t800-b4-s64", L=32, Hq=32, Hkv=32, D=96, V=32064, d=3072, ffn=8192,
                 t=800, b=4, s=64, R=64, W=0, theta=10000.0),
     # configs[2]: request-parallel over 1/2/4/8 GPUs (R per GPU)
-    "llama": dict(name="llama3.1-8b-gqa-humaneval-t150-b8-s256", L=32, Hq=32, Hkv=8, D=128,
+    "llama": dict(name="llama3.1-8b-gqa-humaneval-t150-b8-s256", L=32, Hq=32, Hkv=8, D=128, d=4096, ffn=14336,
                   V=128256, t=150, b=8, s=256, R=32, W=0, theta=500000.0),
     # configs[3]: Mistral-Small-24B-shaped SWA, W = 4096 (reading A15); the 8 KV heads are
     # sharded over the N ranks (8/N KV heads + their 32/N query heads each, the SAME R
     # requests on every rank) with a per-layer all-gather of the attention outputs
     # (paper_2502_00085_b200/dist.py); strong scaling: the job is fixed, N = 1 holds all heads
-    "mistral-shard": dict(name="mistral-small-24b-swa-t4096-b4-s128-kvshard", L=40, Hq=32, Hkv=8,
+    "mistral-shard": dict(name="mistral-small-24b-swa-t4096-b4-s128-kvshard", L=40, Hq=32, Hkv=8, d=5120, ffn=32768,
                           D=128, V=131072, t=4096, b=4, s=128, R=16, W=4096, theta=1e8, kv_shard=True),
     # configs[4] kernel-level sweep point (b set by --beam)
     "sweep": dict(name="llama3.1-8b-gqa-t8192-sweep", L=4, Hq=32, Hkv=8, D=128, V=128256, t=8192,
@@ -835,6 +835,8 @@ def run_gpu(args):
         res["series"] = run_series(hp, advance_to)
     if not args.no_e2e:
         res["e2e"] = run_e2e(hp, args, world)
+    if args.model_context:  # last: it drives the trie with the model's own logits
+        res["model_context"] = run_model_context(hp, args, world)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -850,10 +852,28 @@ def run_series(hp, advance_to):
     torch = hp.torch
     advance_to(0)
     torch.cuda.synchronize()
-    out = dict(k=[], attn_ms=[], beam_ms=[], gc_ms=[], gc_ran=[], trie_rows=[], batch_rows=[])
+    out = dict(k=[], attn_ms=[], beam_ms=[], gc_ms=[], gc_ran=[], trie_rows=[], batch_rows=[],
+               dead_rows=[], dead_tiles=[], tiles=[])
     for i in range(hp.s):
         k = hp.k
         rows = int(hp.st.n_nodes.sum().item()) if k > 0 else hp.R * hp.t
+        # g > 1: generated rows no live beam sees (mask 0) and 64-row tiles made only of them
+        # (the tiles a dead-tile skip could avoid; every depth keeps >= 1 live ancestor, so a
+        # tile spanning >= 1 whole step of b <= 64 appended rows always holds a live row)
+        dr = dt = nt = 0
+        if k > 0:
+            N = hp.st.n_nodes.cpu().numpy()
+            msk = hp.st.beam_mask.cpu().numpy()
+            for r in range(hp.R):
+                gen = msk[r, hp.t: N[r]]
+                dr += int(np.count_nonzero(gen == 0))
+                for t0 in range(0, int(N[r]), 64):
+                    nt += 1
+                    if t0 >= hp.t and not np.any(msk[r, t0: min(t0 + 64, N[r])]):
+                        dt += 1
+        out["dead_rows"].append(dr)
+        out["dead_tiles"].append(dt)
+        out["tiles"].append(nt)
         key = hp.next_key()
         hp.replay(i % 2, timed=True)
         torch.cuda.synchronize()
@@ -876,9 +896,128 @@ def run_series(hp, advance_to):
         gc_ms_mean=round(float(gc.mean()), 4) if len(gc) else None,
         pass_ms_mean=round(float(pas.mean()), 4),
         gc_over_pass_max=round(float((np.array(out["gc_ms"]) / pas).max()), 4),
+        dead_rows_mean=round(float(np.mean(out["dead_rows"])), 1),
+        dead_tiles_total=int(np.sum(out["dead_tiles"])), tiles_total=int(np.sum(out["tiles"])),
         note="rows = KV entries (one per token per layer set); trie rows before each step, "
              "batch = b (t + k) per request (prompt replicated, P:42 counting)")
     return out
+
+
+def run_model_context(hp, args, world):
+    """--model-context: the same job with the random-init model around the hot path
+    (paper_2502_00085_b200.model.ShapedModel: bf16 cuBLAS GEMMs for Q/K/V, O, MLP and LM
+    head, the library's fused RoPE + append + trie attention per layer, the beam step on
+    the model's own fp32 logits, GC), replayed as CUDA graphs.  Reports request-steps/s of
+    the whole decode step and its breakdown (event nodes around every attention launch,
+    the LM head, the beam step and GC; the rest is the layers' GEMMs and elementwise ops).
+    SURVEY §8(d): "Report the breakdown: GEMM / attn / beam-step / prune"."""
+    import torch
+
+    from paper_2502_00085_b200.dist import gather_heads, heads_view
+    from paper_2502_00085_b200.model import ShapedModel
+    wl = hp.wl
+    if "d" not in wl:
+        raise SystemExit("--model-context: phi, llama or mistral-shard")
+    m = ShapedModel(hp.L, wl["d"], wl["Hq"], wl["Hkv"], hp.D, wl["ffn"], hp.V, wl["theta"],
+                    kappa=float(wl.get("kappa", 3.0)), q_heads=hp.Hq, kv_heads=hp.Hkv)
+    st, L = hp.st, hp.L
+    gather = None
+    if hp.kv_shard and world > 1:
+        def gather(o):
+            if hp.eager:
+                return heads_view(gather_heads(o.cpu())).to(o.device)
+            dst = hp.gathered if o.shape[1] == hp.b else hp.gathered1
+            return heads_view(gather_heads(o, dst))
+
+    def step(var, events=None):
+        if var == "first":
+            st.reset()
+        lg = m.step(st, hp.kp, hp.vp, gather=gather, events=None if events is None else events[:L + 1])
+        if events is not None:
+            events[L + 1][0].record()
+        st.beam_step(lg, hp.sel_p, hp.sel_t, hp.sel_s)
+        if events is not None:
+            events[L + 1][1].record()
+            events[L + 2][0].record()
+        st.prune_compact(hp.kp, hp.vp)
+        if events is not None:
+            events[L + 2][1].record()
+
+    ev = {v: [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+              for _ in range(L + 3)] for v in ("first", "steady")}
+    step("first")
+    step("steady")
+    torch.cuda.synchronize()
+    graphs = {}
+    for var in ("first", "steady"):
+        for timed in (False, True):
+            if hp.eager:
+                graphs[(var, timed)] = _Eager(lambda var=var, timed=timed: step(var, ev[var] if timed else None))
+                continue
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                step(var, ev[var] if timed else None)
+            graphs[(var, timed)] = gr
+    k = [0]
+
+    def replay(timed=False):
+        var = "first" if k[0] == 0 else "steady"
+        graphs[(var, timed)].replay()
+        k[0] = (k[0] + 1) % hp.s
+        return var
+    for _ in range(args.warmup):
+        replay()
+    if args.steps < hp.s:
+        while k[0] != (hp.s - args.steps) // 2:
+            replay()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k_first = k[0]
+    t0.record()
+    for _ in range(args.steps):
+        replay()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device=hp.dev if not hp.eager else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    # breakdown over the same job steps of the next job (instrumented graphs, synced per step)
+    while k[0] != k_first:
+        replay()
+    attn, lm, beam, gc, tot = [], [], [], [], []
+    for _ in range(args.steps):
+        a = torch.cuda.Event(enable_timing=True)
+        z = torch.cuda.Event(enable_timing=True)
+        a.record()
+        var = replay(timed=True)
+        z.record()
+        torch.cuda.synchronize()
+        e = ev[var]
+        attn.append(sum(e[l][0].elapsed_time(e[l][1]) for l in range(L)))
+        lm.append(e[L][0].elapsed_time(e[L][1]))
+        beam.append(e[L + 1][0].elapsed_time(e[L + 1][1]))
+        gc.append(e[L + 2][0].elapsed_time(e[L + 2][1]))
+        tot.append(a.elapsed_time(z))
+    assert st.status() == 0, f"device status bits {st.status():#x}"
+    step_ms = ms / args.steps
+    f = step_ms / float(np.mean(tot))  # scale the instrumented step to the plain one
+    N = st.n_nodes.cpu().numpy()
+    units = hp.R if hp.kv_shard else hp.R * world
+    br = dict(attention=float(np.mean(attn)) * f, lm_head=float(np.mean(lm)) * f,
+              beam_step=float(np.mean(beam)) * f, gc=float(np.mean(gc)) * f)
+    br["layer_gemms_and_elementwise"] = step_ms - sum(br.values())
+    return dict(value=round(units * args.steps / (ms * 1e-3), 2), unit="request-steps/s",
+                ms_per_step=round(step_ms, 4), weights_GB=round(m.weight_bytes() / 1e9, 2),
+                logit_scale=m.kappa,
+                breakdown_ms_per_step={k_: round(v, 4) for k_, v in br.items()},
+                trie_rows_end=int(N.sum()),
+                model="random-init bf16 decoder of the workload's shape (cuBLAS GEMMs via torch; "
+                      "prompt K/V rows synthetic); the library runs attention, beam step and GC",
+                timing=f"{args.steps} CUDA-graph replays (job steps {k_first}..); breakdown from "
+                       "event-instrumented replays of the same job steps, scaled to the plain step")
 
 
 def run_e2e(hp, args, world):
@@ -1199,6 +1338,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--series", action="store_true",
                     help="NEXT-1 experiments: one whole instrumented job, per-step times and rows")
+    ap.add_argument("--model-context", action="store_true",
+                    help="also time the step inside a random-init model of the workload's shape")
     ap.add_argument("--prompt-len", type=int, default=0)
     ap.add_argument("--new-tokens", type=int, default=0)
     ap.add_argument("--logit-scale", type=float, default=0.0,

@@ -115,3 +115,99 @@ class TinyModel:
             x = x + o.view(R * b, -1) @ lw["wo"]
             x = self._mlp(x, lw)
         return self._logits(x).view(R, b, self.V)
+
+
+class ShapedModel:
+    """Random-init bf16 decoder shaped like Phi-3.5-mini / Llama-3.1-8B / Mistral-Small-24B
+    (north_star: "model GEMMs ... random-init MHA, GQA and SWA layers shaped like ...,
+    using cuBLAS ... context, not product").  One decode step of the b_live leaves:
+
+        x = E[token of each leaf];  per layer:  h = rmsnorm(x) g1;  q, k, v = h Wq, h Wk, h Wv
+        (cuBLAS);  trie_attn_decode_rope (the library: RoPE at trie depth, append, trie
+        attention);  x += o Wo;  x += (silu(h2 Wg) * (h2 Wu)) Wd with h2 = rmsnorm(x) g2;
+        logits = kappa * (rmsnorm(x) gf) W_lm  (fp32, [R][b_live][V]).
+
+    Weights are N(0, 1 / fan_in) bf16 from a seeded torch generator; every buffer is
+    preallocated per b_live so a step is CUDA-graph capturable.  The prompt's K/V rows are
+    whatever the caller put in the pools (the bench's synthetic prompt rows)."""
+
+    def __init__(self, L, d, Hq, Hkv, D, ffn, V, rope_base, kappa=3.0, eps=1e-5, seed=0,
+                 device="cuda", q_heads=None, kv_heads=None):
+        g = torch.Generator(device=device)
+        g.manual_seed(0x7472696500 + seed)
+        self.L, self.d, self.D, self.ffn, self.V = L, d, D, ffn, V
+        # local heads (KV-head shard: this rank's slice); O-proj reads all Hq heads
+        self.Hq_all, self.Hq, self.Hkv = Hq, q_heads or Hq, kv_heads or Hkv
+        self.base, self.kappa, self.eps = rope_base, kappa, eps
+
+        def W(n_in, n_out):
+            return (torch.randn(n_in, n_out, generator=g, device=device, dtype=torch.bfloat16)
+                    * (1.0 / math.sqrt(n_in))).to(torch.bfloat16)
+        self.layers = []
+        for _ in range(L):
+            self.layers.append(dict(
+                wq=W(d, self.Hq * D), wk=W(d, self.Hkv * D), wv=W(d, self.Hkv * D),
+                wo=W(Hq * D, d), wgu=W(d, 2 * ffn), wd=W(ffn, d),
+                g1=torch.ones(d, device=device, dtype=torch.bfloat16),
+                g2=torch.ones(d, device=device, dtype=torch.bfloat16)))
+        self.emb = torch.randn(V, d, generator=g, device=device, dtype=torch.bfloat16)
+        self.lm = W(d, V)
+        self.gf = torch.ones(d, device=device, dtype=torch.bfloat16)
+        self.device = device
+        self.bufs = {}
+
+    def weight_bytes(self):
+        n = self.emb.numel() + self.lm.numel() + self.gf.numel()
+        for lw in self.layers:
+            n += sum(t.numel() for t in lw.values())
+        return 2 * n
+
+    def _buf(self, R, b):
+        key = (R, b)
+        if key not in self.bufs:
+            M, dev, bf = R * b, self.device, torch.bfloat16
+            self.bufs[key] = dict(
+                q=torch.empty(R, b, self.Hq, self.D, device=dev, dtype=bf),
+                k=torch.empty(R, b, self.Hkv, self.D, device=dev, dtype=bf),
+                v=torch.empty(R, b, self.Hkv, self.D, device=dev, dtype=bf),
+                o=torch.empty(R, b, self.Hq, self.D, device=dev, dtype=bf),
+                logits=torch.empty(R, b, self.V, device=dev, dtype=torch.float32))
+        return self.bufs[key]
+
+    def _norm(self, x, g):
+        xf = x.float()
+        return (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + self.eps)).to(x.dtype) * g
+
+    @torch.no_grad()
+    def step(self, st, k_pools, v_pools, gather=None, events=None):
+        """One decode step's forward for the handle's b_live leaves; returns the fp32 logits
+        buffer [R][b_live][V].  gather(o) -> [R][b][Hq_all][D] (KV-head shard; None: o).
+        events: optional list of (start, end) CUDA event pairs, one per layer's attention
+        launch, + one for the LM head."""
+        R, b = st.R, st.b_live
+        B = self._buf(R, b)
+        tok = torch.gather(st.token, 1, st.leaf[:, :b].long()).view(-1).long()
+        x = self.emb.index_select(0, tok)                      # [R*b][d]
+        for l, lw in enumerate(self.layers):
+            h = self._norm(x, lw["g1"])
+            torch.mm(h, lw["wq"], out=B["q"].view(R * b, -1))
+            torch.mm(h, lw["wk"], out=B["k"].view(R * b, -1))
+            torch.mm(h, lw["wv"], out=B["v"].view(R * b, -1))
+            if events is not None:
+                events[l][0].record()
+            st.attn_decode_rope(B["q"], B["k"], B["v"], k_pools[l], v_pools[l], self.base, B["o"])
+            if events is not None:
+                events[l][1].record()
+            o = B["o"] if gather is None else gather(B["o"])
+            x = x + torch.mm(o.reshape(R * b, -1), lw["wo"])
+            h2 = self._norm(x, lw["g2"])
+            gu = torch.mm(h2, lw["wgu"])
+            x = x + torch.mm(torch.nn.functional.silu(gu[:, : self.ffn]) * gu[:, self.ffn:], lw["wd"])
+        if events is not None:
+            events[self.L][0].record()
+        lg = torch.mm(self._norm(x, self.gf), self.lm)
+        B["logits"].view(R * b, -1).copy_(lg)
+        B["logits"].mul_(self.kappa)
+        if events is not None:
+            events[self.L][1].record()
+        return B["logits"]
