@@ -244,6 +244,15 @@ class HotPath:
                          if self.kv_shard and world > 1 else None)
         self.gathered1 = (torch.empty(world, R, 1, Hq, D, dtype=torch.bfloat16, device=dev)
                           if self.gathered is not None else None)
+        # NEXT-4 (default for the KV-head shard at N > 1): the all-gather fused into the
+        # attention kernels -- peer stores from the epilogue into every rank's gather buffer
+        # (CUDA IPC / NVLink), a flag per rank, trie_gather_wait; BENCH_GATHER=nccl keeps the
+        # NCCL all_gather_into_tensor per layer instead
+        self.fg = None
+        if self.gathered is not None and os.environ.get("BENCH_GATHER", "fused") == "fused":
+            self.fg = tdist.FusedGather(self.st, world, rank)
+            self.gathered = torch.empty(R, b, world * Hq, D, dtype=torch.bfloat16, device=dev)
+            self.gathered1 = torch.empty(R, 1, world * Hq, D, dtype=torch.bfloat16, device=dev)
         self.sel_p = torch.empty(R, b, dtype=torch.int32, device=dev)
         self.sel_t = torch.empty_like(self.sel_p)
         self.sel_s = torch.empty(R, b, dtype=torch.float32, device=dev)
@@ -306,6 +315,9 @@ class HotPath:
         from paper_2502_00085_b200.dist import gather_heads
         # the first step of a job has one live beam: its own buffer
         dst = self.gathered if out.shape[1] == self.b else self.gathered1
+        if self.fg is not None:  # fused: the kernel already stored into every rank's buffer
+            self.fg.wait(dst)
+            return
         if self.eager:  # gloo: through host memory
             dst.copy_(gather_heads(out.cpu()))
             return

@@ -263,6 +263,50 @@ int trie_batch_reorder_kv(int32_t n_requests, int32_t beam_width, int32_t n_laye
                           void* const* dst_k_host, void* const* dst_v_host, uint32_t* status,
                           cudaStream_t stream);
 
+/*
+ * the KV-head shard's per-layer all-gather of attention
+ * outputs FUSED into trie_attn_decode_rope (BASELINE.json configs[3]; the paper's
+ * multi-GPU run, states no mechanism).  World W <= 8 ranks hold the same requests
+ * and trie (identical logits -> identical selections) but each only its KV heads
+ * [rank*Hkv, (rank+1)*Hkv) and their Hq query heads (cfg.n_q_heads / n_kv_heads are the
+ * LOCAL counts).  Every rank owns a gather buffer of 2 halves, each [R][b_live][W*Hq][D]
+ * (dtype of the pools), and a flag array uint32 [W]; both are exchanged between the
+ * processes (trie_ipc_alloc / trie_ipc_open: CUDA IPC -- peer-mapped over NVLink on an
+ * 8-GPU box, the same device on a one-GPU test box).
+ *
+ * trie_gather_setup registers, for every rank p, this process's pointer to p's gather
+ * buffer and to p's flag array (peer_out_host[rank] / peer_flags_host[rank] = the local
+ * ones).  From then on every trie_attn_decode_rope call on the handle, in the epilogue of
+ * the kernel that produces the output rows (the attention kernel, or the split-K combine),
+ * also stores every output row of its heads into EVERY rank's gather buffer (head block
+ * `rank`, half = the call's sequence number mod 2; the local `out` is written as before)
+ * with plain peer stores as each CTA finishes, then -- after the last output row of the
+ * launch -- publishes the launch's sequence number e (1, 2, ...) to flags[rank] of every
+ * rank (release, system scope).  Every rank must make the same sequence of calls.
+ * trie_gather_wait enqueues a wait until every rank's flag in the LOCAL flag array reaches
+ * this rank's own e (acquire, system scope) and then copies half (e - 1) mod 2 of the local
+ * gather buffer -- every rank's heads of call e, [R][b_live][W*Hq][D] -- into gathered_out
+ * (device; NULL: wait only).  Two halves (each R*beam_width*W*Hq*D elements): a rank can
+ * run one call ahead of a slower peer still reading the previous call's half; it cannot
+ * run two ahead, since its next wait needs that peer's next call.  Both the sequence
+ * number and the half are device-side, so the calls are CUDA-graph replayable.
+ * Supported on the fused bf16 tensor-core paths (trie_attn_plan_info [2] = 1); EINVAL
+ * otherwise.  world = 1 (or setup never called) disables the gather.
+ */
+int trie_gather_setup(trie_handle* h, int32_t world, int32_t rank, void* const* peer_out_host,
+                      uint32_t* const* peer_flags_host);
+int trie_gather_wait(trie_handle* h, void* gathered_out, cudaStream_t stream);
+
+/*
+ * CUDA IPC helpers for the gather buffers: trie_ipc_alloc = cudaMalloc (zeroed) + its
+ * 64-byte cudaIpcMemHandle_t in handle_out; trie_ipc_open maps a peer's handle into this
+ * process (cudaIpcMemLazyEnablePeerAccess); trie_ipc_close / trie_ipc_free undo them.
+ */
+int trie_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out);
+int trie_ipc_open(const void* handle, void** dev_ptr);
+int trie_ipc_close(void* dev_ptr);
+int trie_ipc_free(void* dev_ptr);
+
 /* Read (and keep) the latched device status bits.  Synchronises the stream. */
 int trie_status(trie_handle* h, uint32_t* bits_host, cudaStream_t stream);
 

@@ -23,7 +23,8 @@ SYMBOLS = ["trie_workspace_bytes", "trie_create", "trie_reset", "trie_destroy", 
            "trie_rope_kv_append", "trie_attn_scratch_bytes", "trie_attn_decode", "trie_beam_step",
            "trie_append", "trie_prune_compact", "trie_read_hyps", "trie_status", "trie_last_error",
            "trie_version", "trie_launch_count", "trie_attn_decode_rope", "trie_attn_plan_info",
-           "trie_batch_reorder_kv", "trie_set_eos"]
+           "trie_batch_reorder_kv", "trie_set_eos", "trie_gather_setup", "trie_gather_wait",
+           "trie_ipc_alloc", "trie_ipc_open", "trie_ipc_close", "trie_ipc_free"]
 
 
 class trie_cfg(ctypes.Structure):
@@ -75,6 +76,12 @@ def load(path: str = LIB_PATH):
         "trie_launch_count": (ctypes.c_ulonglong, []),
         "trie_batch_reorder_kv": (ctypes.c_int, [I32] * 7 + [P] * 3 + [P] * 4 + [P, P]),
         "trie_set_eos": (ctypes.c_int, [P, I32]),
+        "trie_gather_setup": (ctypes.c_int, [P, I32, I32, P, P]),
+        "trie_gather_wait": (ctypes.c_int, [P, P, P]),
+        "trie_ipc_alloc": (ctypes.c_int, [SZ, ctypes.POINTER(P), P]),
+        "trie_ipc_open": (ctypes.c_int, [P, ctypes.POINTER(P)]),
+        "trie_ipc_close": (ctypes.c_int, [P]),
+        "trie_ipc_free": (ctypes.c_int, [P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -240,3 +247,56 @@ def trie_attn_plan_info(cfg: trie_cfg, b_live: int, rows_hint: int = 0) -> dict:
     _check(load().trie_attn_plan_info(ctypes.byref(cfg), b_live, rows_hint, ctypes.cast(info, ctypes.c_void_p)),
            "trie_attn_plan_info")
     return dict(path=ATTN_PATHS.get(info[0], str(info[0])), splits=info[1], fused_rope=bool(info[2]), Qg=info[3])
+
+
+# ---- NEXT-4: fused KV-head-shard all-gather (trie_gather_setup) ---------------------------
+def trie_gather_setup(h, world: int, rank: int, peer_out, peer_flags):
+    """peer_out / peer_flags: sequences of `world` device pointers (ints) or CUDA tensors --
+    every rank's gather buffer and flag array as mapped in this process."""
+    outs = (ctypes.c_void_p * max(world, 1))(*[_ptr(x) for x in peer_out])
+    flags = (ctypes.c_void_p * max(world, 1))(*[_ptr(x) for x in peer_flags])
+    _check(load().trie_gather_setup(h, world, rank, ctypes.cast(outs, ctypes.c_void_p),
+                                    ctypes.cast(flags, ctypes.c_void_p)), "trie_gather_setup")
+
+
+def trie_gather_wait(h, gathered_out=None, stream=None):
+    _check(load().trie_gather_wait(h, _ptr(gathered_out), _stream(stream)), "trie_gather_wait")
+
+
+def trie_ipc_alloc(nbytes: int):
+    """cudaMalloc'd, zeroed, IPC-exportable device memory: (device pointer, 64-byte handle)."""
+    ptr = ctypes.c_void_p()
+    hd = ctypes.create_string_buffer(64)
+    _check(load().trie_ipc_alloc(nbytes, ctypes.byref(ptr), ctypes.cast(hd, ctypes.c_void_p)), "trie_ipc_alloc")
+    return int(ptr.value), bytes(hd.raw)
+
+
+def trie_ipc_open(handle: bytes) -> int:
+    ptr = ctypes.c_void_p()
+    hd = ctypes.create_string_buffer(handle, 64)
+    _check(load().trie_ipc_open(ctypes.cast(hd, ctypes.c_void_p), ctypes.byref(ptr)), "trie_ipc_open")
+    return int(ptr.value)
+
+
+def trie_ipc_close(ptr: int):
+    _check(load().trie_ipc_close(ptr), "trie_ipc_close")
+
+
+def trie_ipc_free(ptr: int):
+    _check(load().trie_ipc_free(ptr), "trie_ipc_free")
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (the IPC buffers) for torch."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = dict(shape=tuple(shape), typestr=typestr, data=(int(ptr), False),
+                                             version=3, strides=None)
+
+
+def device_tensor(ptr: int, shape, dtype):
+    """A torch tensor aliasing device memory at ptr (no copy; the memory stays owned by the
+    library's trie_ipc_* calls)."""
+    ts = {torch.bfloat16: "<i2", torch.int32: "<i4", torch.float32: "<f4"}[dtype]
+    t = torch.as_tensor(_CudaArray(ptr, shape, ts), device="cuda")
+    return t.view(dtype) if dtype == torch.bfloat16 else t

@@ -111,6 +111,7 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
   char* ss = take(R * b * 4);
   char* rtab = take(R * TRIE_MAX_BEAMS * (c->head_dim / 2) * 8);
   char* fin = take(R * TRIE_MAX_BEAMS * 4);
+  char* gat = take(64);  // gather ticket + completed-launch counter (NEXT-4)
   if (h) {
     h->token = (int32_t*)token;
     h->parent = (int32_t*)parent;
@@ -139,6 +140,8 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
     h->sel_score = (float*)ss;
     h->rope_tab = (float2*)rtab;
     h->fin = (uint32_t*)fin;
+    h->g_ticket = (uint32_t*)gat;
+    h->g_epoch = (uint32_t*)gat + 1;
     h->chunks = (int32_t)chunks;
   }
   return off;
@@ -192,6 +195,7 @@ int trie_create(const trie_cfg* cfg, void* workspace, size_t workspace_bytes,
                         (size_t)cfg->n_requests * cfg->max_prompt_len * 4,
                         cudaMemcpyDeviceToDevice, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->status, 0, 4, stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->g_ticket, 0, 8, stream);  // ticket, epoch
   if (e == cudaSuccess)
     e = cudaMemsetAsync(h->cnt_row, 0, (size_t)cfg->n_requests * (TRIE_MAX_BEAMS + 1) * 4, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // prompt_lens_host may be freed
@@ -416,6 +420,8 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.rope_tab = h->rope_tab;
   const bool fuse = trie::attn_rope_fusable(p) &&
                     (((uintptr_t)q | (uintptr_t)k_new | (uintptr_t)v_new) & 3) == 0;
+  if (h->g_world > 1 && !fuse)
+    return trie_set_error(TRIE_EINVAL, "gather: needs the fused bf16 tensor-core path");
   if (!fuse) {  // two launches: rotate + append, then attention over the handle's trie
     int rc = trie::launch_rope_append(h, const_cast<void*>(q), const_cast<void*>(k_new), v_new,
                                       k_pool, v_pool, rope_theta, stream);
@@ -441,6 +447,11 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.splits = pl.splits;
   // NEXT-3: with an EOS id, the fused kernels skip requests whose beams all finished
   if (h->eos >= 0) p.fin = h->fin;
+  if (h->g_world > 1) {  // NEXT-4: the output rows also go to every rank's gather buffer
+    p.ga = trie_gather_args(h);
+    const uint32_t items = (uint32_t)(cfg->n_requests * cfg->n_kv_heads);
+    p.ga.expected = pl.splits == 1 ? items : items * (uint32_t)(b_live * (cfg->n_q_heads / cfg->n_kv_heads));
+  }
   if (cfg->window == 0 && prefetch_enabled()) {
     // tiles below the shortest prompt's last row hold prompt rows that no kernel of the
     // library writes (AttnParams::pre_tiles); row t - 1 is excluded: it is the first

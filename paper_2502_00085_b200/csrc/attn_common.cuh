@@ -4,6 +4,19 @@
 
 namespace trie {
 
+// NEXT-4 fused all-gather of the KV-head shard (trie_gather_setup): every output row is
+// also stored into every rank's gather buffer; the last item of the launch publishes the
+// launch's sequence number to every rank's flag array.  world == 0: disabled.
+struct GatherArgs {
+  void* out[8];       // per rank: its gather buffer [2][R][b_live][world*Hq][D] (bf16)
+  uint32_t* flag[8];  // per rank: its flag array [world]
+  uint32_t* ticket;   // this handle's arrival counter (zero between launches)
+  uint32_t* epoch;    // this handle's completed-launch counter
+  int world, rank;
+  uint32_t expected;  // arrivals per launch (items, or rows for the split-K combine)
+  size_t half_stride; // elements per half: R * beam_width * world * Hq * D
+};
+
 struct AttnParams {
   const void* q;       // [R][b_live][Hq][D]
   const void* k;       // [R][Hkv][cap][D]
@@ -39,9 +52,11 @@ struct AttnParams {
   // NEXT-3 (narrow / wide, handle path with an EOS id): fin [R][32] finished flags; a
   // request whose b_live beams are all finished is done -- its CTAs read and write nothing
   const uint32_t* fin;
+  GatherArgs ga;
 };
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);
+int launch_gather_wait(const GatherArgs& ga, int R, int b_live, int Hq, int D, void* dst, cudaStream_t s);
 int launch_attn_tc(const AttnParams& p, cudaStream_t s);
 bool attn_rope_fusable(const AttnParams& p);
 bool attn_tc_supported(const AttnParams& p);

@@ -17,6 +17,7 @@
 #include "attn_common.cuh"
 #include "common.cuh"
 #include "handle.h"
+#include "gather.cuh"
 
 namespace trie {
 
@@ -186,9 +187,14 @@ __global__ void __launch_bounds__(128) k_attn_combine(const AttnParams p) {
   if (gw >= total) return;
   const int m = gw % Qg, h = (gw / Qg) % p.Hkv, r = gw / (Qg * p.Hkv);
   const int D = p.D;
+  // NEXT-4 fused all-gather (bf16): one arrival per combined row
+  constexpr bool kBf16 = sizeof(T) == 2;
+  const bool gat = kBf16 && p.ga.world > 0;
   if (p.fin != nullptr &&  // NEXT-3: a finished request's splits wrote nothing; neither do we
-      __all_sync(0xffffffffu, lane >= p.b_live || p.fin[r * TRIE_MAX_BEAMS + lane] != 0u))
+      __all_sync(0xffffffffu, lane >= p.b_live || p.fin[r * TRIE_MAX_BEAMS + lane] != 0u)) {
+    if (gat && lane == 0) gather_arrive(p);
     return;
+  }
   const float* base = p.part + (((size_t)r * p.Hkv + h) * p.splits * Qg) * (D + 2);
   // lanes own splits (<= 64): (m_s, l_s) loaded in parallel, weights w_s = 2^(m_s - M)
   float ms[2], ls[2];
@@ -230,12 +236,22 @@ __global__ void __launch_bounds__(128) k_attn_combine(const AttnParams p) {
       }
     }
   }
+  const uint32_t ghalf = gat ? gather_half(p) : 0u;
 #pragma unroll
   for (int c = 0; c < DC; ++c)
-    if (lane + 32 * c < D) op[lane + 32 * c] = from_f<T>(acc[c] * inv);
+    if (lane + 32 * c < D) {
+      const T v = from_f<T>(acc[c] * inv);
+      op[lane + 32 * c] = v;
+      if constexpr (kBf16)
+        if (gat) gather_st16(p, ghalf, r, j, h * g + ii, lane + 32 * c, v);
+    }
   if (p.lse && lane == 0)
     p.lse[((size_t)r * p.b_live + j) * p.Hq + h * g + ii] =
         L > 0.f ? (M + log2f(L)) * 0.69314718055994531f : -INFINITY;
+  if (gat) {
+    __syncwarp();
+    if (lane == 0) gather_arrive(p);
+  }
 }
 
 template <typename T>

@@ -31,6 +31,7 @@
 #include "common.cuh"
 #include "handle.h"
 #include "tc_common.cuh"
+#include "gather.cuh"
 
 namespace trie {
 
@@ -344,7 +345,11 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
     if (lane == 0) mbar_arrive(&empty[s]);
   }
   ATTN_TRC(lane == 0, 3);
-  if (it.done) return;  // NEXT-3: finished request, output not written
+  const bool gat = p.ga.world > 0 && p.splits == 1;  // NEXT-4: fused all-gather
+  if (it.done) {  // NEXT-3: finished request, output not written
+    if (gat && lane == 0) gather_arrive(p);
+    return;
+  }
   // ---- epilogue: column sums over the 8 lanes of a column quad, transpose via smem ----
 #pragma unroll
   for (int nq = 0; nq < NQ; ++nq)
@@ -379,14 +384,18 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
   }
   __syncwarp();
   const int nqr = min(Qg, NQ * 8);
+  const uint32_t ghalf = gat ? gather_half(p) : 0u;
   for (int m = 0; m < nqr; ++m) {
     const float M = stage_out[m * RW + D], Ls = stage_out[m * RW + D + 1];
     const int j = m / g, ii = m % g;
     if (p.splits == 1) {
       __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
       const float inv = Ls > 0.f ? 1.f / Ls : 0.f;
-      for (int d = lane * 2; d < D; d += 64)
-        *(uint32_t*)(op + d) = pack_bf16(stage_out[m * RW + d] * inv, stage_out[m * RW + d + 1] * inv);
+      for (int d = lane * 2; d < D; d += 64) {
+        const uint32_t v = pack_bf16(stage_out[m * RW + d] * inv, stage_out[m * RW + d + 1] * inv);
+        *(uint32_t*)(op + d) = v;
+        if (gat) gather_st32(p, ghalf, r, j, h * g + ii, d, v);
+      }
       if (lane == 0) {
         if (Ls == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
         if (p.lse)
@@ -401,6 +410,10 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
         pp[D + 1] = Ls;
       }
     }
+  }
+  if (gat) {  // the item's rows are stored (this warp wrote all of them)
+    __syncwarp();
+    if (lane == 0) gather_arrive(p);
   }
   ATTN_TRC(lane == 0, 4);
 }
@@ -724,7 +737,18 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       }
     }
   }
-  if (it.done) return;  // NEXT-3: finished request, output not written
+  // NEXT-4 fused all-gather: the MT writer warps (row slice 0) meet at named barrier 3,
+  // then one lane arrives for the item
+  const bool gat = p.ga.world > 0 && p.splits == 1;
+  if (it.done) {  // NEXT-3: finished request, output not written
+    if (gat) {
+      __syncwarp();
+      asm volatile("bar.sync 3, %0;" ::"r"(MT * 32) : "memory");
+      if (mt == 0 && lane == 0) gather_arrive(p);
+    }
+    return;
+  }
+  const uint32_t ghalf = gat ? gather_half(p) : 0u;
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int m = qm[u];
@@ -734,8 +758,11 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
       const float inv = lrow[u] > 0.f ? 1.f / lrow[u] : 0.f;
 #pragma unroll
-      for (int dt = 0; dt < C::DT; ++dt)
-        *(uint32_t*)(op + dt * 8 + cq * 2) = pack_bf16(o[dt][u * 2] * inv, o[dt][u * 2 + 1] * inv);
+      for (int dt = 0; dt < C::DT; ++dt) {
+        const uint32_t v = pack_bf16(o[dt][u * 2] * inv, o[dt][u * 2 + 1] * inv);
+        *(uint32_t*)(op + dt * 8 + cq * 2) = v;
+        if (gat) gather_st32(p, ghalf, r, j, h * g + ii, dt * 8 + cq * 2, v);
+      }
       if (cq == 0) {
         if (lrow[u] == 0.f) latch(p.status, TRIE_ST_EMPTY_ROW);
         if (p.lse)
@@ -754,6 +781,11 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
         pp[D + 1] = lrow[u];
       }
     }
+  }
+  if (gat) {
+    __syncwarp();
+    asm volatile("bar.sync 3, %0;" ::"r"(MT * 32) : "memory");
+    if (mt == 0 && lane == 0) gather_arrive(p);
   }
   ATTN_TRC(cw == 0 && lane == 0, 4);
 }

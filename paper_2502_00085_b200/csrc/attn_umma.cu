@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "handle.h"
 #include "tc_common.cuh"
+#include "gather.cuh"
 
 namespace trie {
 
@@ -519,6 +520,8 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
       const int j = beam, ii = row % g;
       constexpr int HD = D / 2;
       const int c0 = grp * HD;
+      const bool gat = p.ga.world > 0 && p.splits == 1;  // NEXT-4 fused all-gather
+      const uint32_t ghalf = gat ? gather_half(p) : 0u;
       if (!trc && !it.done) {  // NEXT-3: a done request (all beams finished) writes nothing
         if (p.splits == 1) {
           __nv_bfloat16* op = (__nv_bfloat16*)p.out + (((size_t)r * p.b_live + j) * p.Hq + h * g + ii) * D;
@@ -541,8 +544,14 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
               for (int k = 0; k < 8; ++k)
                 w[k] = pack_bf16(__uint_as_float(o0[2 * k]) * f0 + __uint_as_float(o1[2 * k]) * f1,
                                  __uint_as_float(o0[2 * k + 1]) * f0 + __uint_as_float(o1[2 * k + 1]) * f1);
-              *(int4*)(op + c0 + c) = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
-              *(int4*)(op + c0 + c + 8) = make_int4((int)w[4], (int)w[5], (int)w[6], (int)w[7]);
+              const int4 v0 = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+              const int4 v1 = make_int4((int)w[4], (int)w[5], (int)w[6], (int)w[7]);
+              *(int4*)(op + c0 + c) = v0;
+              *(int4*)(op + c0 + c + 8) = v1;
+              if (gat) {
+                gather_st128(p, ghalf, r, j, h * g + ii, c0 + c, v0);
+                gather_st128(p, ghalf, r, j, h * g + ii, c0 + c + 8, v1);
+              }
             }
           }
           if (qvalid && grp == 0) {
@@ -577,6 +586,11 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
             pp[D + 1] = l;
           }
         }
+      }
+      if (gat) {  // the 2 * n_live writer warps meet at named barrier 6; one lane arrives
+        __syncwarp();
+        asm volatile("bar.sync 6, %0;" ::"r"(2 * n_live * 32) : "memory");
+        if (sp == 0 && grp == 0 && lane == 0) gather_arrive(p);
       }
     }
   }

@@ -46,6 +46,13 @@ struct trie_handle {
   float rope_tab_theta = 0.f;
   int32_t rope_tab_blive = 0;
   int32_t chunks = 1;
+  // NEXT-4 fused all-gather (trie_gather_setup): every rank's gather buffer / flag array as
+  // mapped in this process; ticket + completed-launch counter in the workspace
+  int32_t g_world = 0, g_rank = 0;
+  void* g_out[8] = {};
+  uint32_t* g_flags[8] = {};
+  uint32_t* g_ticket = nullptr;
+  uint32_t* g_epoch = nullptr;
   // host-tracked state
   int32_t b_live = 1;
   int32_t steps = 0;
@@ -54,6 +61,23 @@ struct trie_handle {
 
 // logits per beam-step chunk CTA (beam_step.cu)
 constexpr int TRIE_BEAM_CHUNK = 8192;
+
+// the kernels' view of the handle's gather registration (attn_common.cuh GatherArgs)
+#include "attn_common.cuh"
+inline trie::GatherArgs trie_gather_args(const trie_handle* h) {
+  trie::GatherArgs ga = {};
+  ga.world = h->g_world;
+  ga.rank = h->g_rank;
+  for (int q = 0; q < h->g_world && q < 8; ++q) {
+    ga.out[q] = h->g_out[q];
+    ga.flag[q] = h->g_flags[q];
+  }
+  ga.ticket = h->g_ticket;
+  ga.epoch = h->g_epoch;
+  ga.half_stride = (size_t)h->cfg.n_requests * h->cfg.beam_width * h->g_world * h->cfg.n_q_heads *
+                   h->cfg.head_dim;
+  return ga;
+}
 
 // carve the workspace; with h == nullptr only computes the size
 size_t trie_layout(const trie_cfg* cfg, trie_handle* h, char* base);

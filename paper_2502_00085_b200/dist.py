@@ -91,3 +91,50 @@ def heads_view(gathered: torch.Tensor) -> torch.Tensor:
     """[world][R][b][Hq/world][D] -> [R][b][Hq][D] in global head order (a copy)."""
     w, R, b, hl, D = gathered.shape
     return gathered.permute(1, 2, 0, 3, 4).reshape(R, b, w * hl, D)
+
+
+class FusedGather:
+    """the KV-head shard's per-layer all-gather fused into the attention
+    kernels (include/triedecode.h trie_gather_setup).  Every rank allocates its gather buffer
+    [2][R][b][world*Hq_local][D] bf16 and flag array [world] uint32 with CUDA IPC, the
+    handles are exchanged once over the process group (any backend: plumbing, not data
+    path), every rank maps every peer's buffers and registers them with its trie handle.
+    Then each trie_attn_decode_rope stores its output rows straight into every rank's
+    buffer from the kernel epilogue, and wait(dst) = trie_gather_wait copies the completed
+    call's [R][b_live][world*Hq_local][D] into dst once every rank has published it."""
+
+    def __init__(self, st, world: int, rank: int):
+        from . import _lib as L
+        self.L, self.st, self.world, self.rank = L, st, world, rank
+        half = st.R * st.b * world * st.Hq * st.D
+        self.out_ptr, h_out = L.trie_ipc_alloc(2 * half * 2)
+        self.flag_ptr, h_flag = L.trie_ipc_alloc(64)
+        handles = [None] * world
+        dist.all_gather_object(handles, (h_out, h_flag))
+        self.peer_out, self.peer_flags, self.opened = [], [], []
+        for q, (ho, hf) in enumerate(handles):
+            if q == rank:
+                self.peer_out.append(self.out_ptr)
+                self.peer_flags.append(self.flag_ptr)
+                continue
+            po, pf = L.trie_ipc_open(ho), L.trie_ipc_open(hf)
+            self.opened += [po, pf]
+            self.peer_out.append(po)
+            self.peer_flags.append(pf)
+        L.trie_gather_setup(st.h, world, rank, self.peer_out, self.peer_flags)
+        dist.barrier()  # every rank registered before anyone stores into a peer
+
+    def wait(self, dst=None, stream=None):
+        """Enqueue the wait for the last call's gather; copy it into dst [R][b_live][world*Hq][D]."""
+        self.L.trie_gather_wait(self.st.h, dst, stream)
+        return dst
+
+    def close(self):
+        torch.cuda.synchronize()
+        dist.barrier()  # no rank still stores into our buffers
+        for p in self.opened:
+            self.L.trie_ipc_close(p)
+        self.opened = []
+        dist.barrier()
+        self.L.trie_ipc_free(self.out_ptr)
+        self.L.trie_ipc_free(self.flag_ptr)

@@ -52,10 +52,10 @@ def _inputs(c, k, l, bl):
             _bf(synth.normal(seed, st + 3, (R, bl, Hkv, D))))
 
 
-def _rank(rank, world, port, c, q):
+def _rank(rank, world, port, c, q, fused=False):
     import torch.distributed as dist
 
-    from paper_2502_00085_b200.dist import gather_heads, heads_view, kv_head_shard
+    from paper_2502_00085_b200.dist import FusedGather, gather_heads, heads_view, kv_head_shard
     from paper_2502_00085_b200.trie import TrieState
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -66,6 +66,7 @@ def _rank(rank, world, port, c, q):
     cap = (t + b * s + b + 63) // 64 * 64
     st = TrieState(R, b, t, cap, L, nq, nkv, D, V, prompts, lens, window=W, dtype=torch.bfloat16)
     kp, vp = st.new_pools()
+    fg = FusedGather(st, world, rank) if fused else None
     for l in range(L):
         kp[l][:, :, :t] = _bf(synth.normal(c["seed"], 10 + 2 * l, (R, Hkv, t, D)))[:, kv0:kv0 + nkv].cuda()
         vp[l][:, :, :t] = _bf(synth.normal(c["seed"], 11 + 2 * l, (R, Hkv, t, D)))[:, kv0:kv0 + nkv].cuda()
@@ -78,7 +79,12 @@ def _rank(rank, world, port, c, q):
             out = torch.empty(R, bl, nq, D, dtype=torch.bfloat16, device="cuda")
             st.attn_decode_rope(qf[:, :, q0:q0 + nq].contiguous().cuda(), kf[:, :, kv0:kv0 + nkv].contiguous().cuda(),
                                 vf[:, :, kv0:kv0 + nkv].contiguous().cuda(), kp[l], vp[l], c["base"], out)
-            outs.append(heads_view(gather_heads(out.cpu())).float().numpy())
+            if fg is not None:  # NEXT-4: stored by the kernel into every rank's buffer
+                full = torch.empty(R, bl, Hq, D, dtype=torch.bfloat16, device="cuda")
+                fg.wait(full)
+                outs.append(full.float().cpu().numpy())
+            else:
+                outs.append(heads_view(gather_heads(out.cpu())).float().numpy())
         lg = torch.as_tensor(synth.normal(c["seed"], 5000 + k, (R, bl, V)) * 3.0, dtype=torch.float32).cuda()
         sp = torch.empty(R, b, dtype=torch.int32, device="cuda")
         tk, sc = torch.empty_like(sp), torch.empty(R, b, dtype=torch.float32, device="cuda")
@@ -96,13 +102,19 @@ def _rank(rank, world, port, c, q):
         rec.append(dict(outs=outs, sp=sp.cpu().numpy(), tk=tk.cpu().numpy(), sc=sc.cpu().numpy(),
                         lg=lg.cpu().numpy(), same=same))
     status = st.status()
+    if fg is not None:
+        fg.close()
     dist.barrier()
     if rank == 0:
         q.put((rec, status))
     dist.destroy_process_group()
 
 
-def test_kv_head_shard_two_ranks_one_gpu_matches_oracle():
+@pytest.mark.parametrize("fused", [False, True], ids=["host-gather", "fused-peer-stores"])
+def test_kv_head_shard_two_ranks_one_gpu_matches_oracle(fused):
+    """fused=True: SURVEY §8(f) NEXT-4 -- the attention kernels store their output rows
+    straight into both ranks' gather buffers (CUDA IPC on one GPU; peer-mapped over NVLink
+    on a multi-GPU box) and trie_gather_wait hands back the all-head output."""
     need_gpu()
     import torch.multiprocessing as mp
 
@@ -114,7 +126,7 @@ def test_kv_head_shard_two_ranks_one_gpu_matches_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, c, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, c, q, fused)) for r in range(2)]
     for p in procs:
         p.start()
     rec, status = q.get(timeout=600)
@@ -155,11 +167,13 @@ def test_kv_head_shard_two_ranks_one_gpu_matches_oracle():
     assert checked >= s * L * R * b * Hq // 2
 
 
-def test_bench_kv_shard_two_ranks():
+@pytest.mark.parametrize("gather", ["fused", "host"])
+def test_bench_kv_shard_two_ranks(gather):
     """bench.py --workload mistral-shard at N = 2 (two ranks on one GPU, eager gloo test
-    mode): strong scaling, 4 of the 8 KV heads per rank, a per-layer all-gather."""
+    mode): strong scaling, 4 of the 8 KV heads per rank, a per-layer all-gather -- fused
+    into the attention kernels (NEXT-4, the default) or through host memory."""
     need_gpu()
-    env = dict(os.environ, BENCH_DIST_BACKEND="gloo")
+    env = dict(os.environ, BENCH_DIST_BACKEND="gloo", BENCH_GATHER=gather)
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
                           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "mistral-shard",
