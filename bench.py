@@ -137,6 +137,8 @@ def _workload(args):
         wl["name"] += f"-s{args.new_tokens}"
     if getattr(args, "logit_scale", 0.0):
         wl["kappa"] = args.logit_scale
+    if getattr(args, "paged", 0.0):
+        wl["paged"] = args.paged
     wl["g"] = args.gc_interval
     wl["eos_frac"] = args.eos_frac
     return wl
@@ -161,6 +163,8 @@ def bench_config(wl, world):
         cfg["eos_frac"] = wl["eos_frac"]
     if "kappa" in wl:
         cfg["logit_scale"] = wl["kappa"]
+    if wl.get("paged"):
+        cfg["kv_pool"] = f"paged (64-slot pages, prompt + {wl['paged']} x the no-GC generated pages)"
     return cfg
 
 
@@ -208,12 +212,22 @@ class HotPath:
         # request-parallel partition: this rank owns its own R requests (weak scaling);
         # KV-head shard: every rank holds the same R requests
         prompts, lens = synth.prompts(10_000 + (0 if self.kv_shard else rank), R, t, V)
+        # NEXT-2 (--paged f): paged pools of 64-slot pages -- the prompt's pages plus f x the
+        # no-GC worst case of generated pages, shared by all requests (pages are mapped as a
+        # trie grows and returned by GC; TRIE_ST_CAPACITY latches if the pool runs dry)
+        self.n_pages = 0
+        if wl.get("paged"):
+            self.n_pages = R * ((t + 63) // 64 + int(np.ceil(wl["paged"] * (b * s + b) / 64)) + 1)
         self.st = TrieState(R, b, t, self.cap, L, Hq, Hkv, D, V, prompts, lens, window=W,
-                            dtype=torch.bfloat16, device=dev)
+                            dtype=torch.bfloat16, device=dev, n_pages=self.n_pages)
         self.kp, self.vp = self.st.new_pools()
         for l in range(L):  # resident prompt K/V (prefill is model context; synthetic here)
-            self.kp[l][:, :, :t].normal_(generator=gen)
-            self.vp[l][:, :, :t].normal_(generator=gen)
+            if self.n_pages:  # the prompt pages are the first R * ceil(t / 64) pages
+                self.kp[l][: R * ((t + 63) // 64)].normal_(generator=gen)
+                self.vp[l][: R * ((t + 63) // 64)].normal_(generator=gen)
+            else:
+                self.kp[l][:, :, :t].normal_(generator=gen)
+                self.vp[l][:, :, :t].normal_(generator=gen)
         # inputs: 2 slots x {first (1 live beam), steady (b live beams)}; one flat buffer each
         self.NB = 2
         self.inp = {}
@@ -821,6 +835,14 @@ def run_gpu(args):
                                                f"{args.steps} instrumented step graphs "
                                                f"({ms_b / args.steps:.3f} ms/step; includes the "
                                                "event nodes' launch latency)"))
+    if hp.n_pages:  # NEXT-2: the physical peak (the paper's allocator-peak metric)
+        ps = hp.st.page_stats()
+        page_bytes = 64 * L * 2 * hp.Hkv * hp.D * 2
+        res["paged_pool"] = dict(n_pages=ps["n_pages"], peak_pages=ps["peak"], in_use_end=ps["in_use"],
+                                 page_bytes_all_layers=page_bytes, peak_bytes=ps["peak"] * page_bytes,
+                                 batch_physical_bytes=R * b * hp.cap * L * 2 * hp.Hkv * hp.D * 2,
+                                 note="peak pages in use since trie_create (device counter), i.e. over every job of the run; "
+                                      "batch = b private caches of t + s rows per request")
     res["clocks"] = clk
     res["gpu_launches"] = int(launches)
     nh = n_hist.cpu().numpy()
@@ -833,6 +855,8 @@ def run_gpu(args):
     # included: the paper's 21 = 3 x 7 counting); the trie keeps N rows
     res["kv_memory"] = dict(step_in_job=int(k_star), trie_bytes=trie_b, batch_bytes=batch_b,
                             trie_peak_bytes=int(nh.sum(axis=1).max()) * kv_row,
+                            pool_bytes_allocated=int(2 * L * hp.Hkv * hp.D * 2 * (
+                                hp.n_pages * 64 if hp.n_pages else R * hp.cap)),
                             ratio_batch_over_trie=round(batch_b / max(trie_b, 1), 3),
                             bound_b_ts_over_t_s_b_1=round(b * (t + k_star) / (t + k_star + b - 1), 3),
                             # the Fig. 3 analog: logical KV bytes before every timed
@@ -1352,6 +1376,8 @@ def main():
                     help="NEXT-1 experiments: one whole instrumented job, per-step times and rows")
     ap.add_argument("--model-context", action="store_true",
                     help="also time the step inside a random-init model of the workload's shape")
+    ap.add_argument("--paged", type=float, default=0.0,
+                    help="NEXT-2: paged KV pools sized prompt + f x the no-GC generated pages")
     ap.add_argument("--prompt-len", type=int, default=0)
     ap.add_argument("--new-tokens", type=int, default=0)
     ap.add_argument("--logit-scale", type=float, default=0.0,

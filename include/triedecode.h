@@ -76,7 +76,29 @@ typedef struct trie_cfg {
   int32_t window;         /* W: sliding window in keys incl. self along the branch; 0 = dense */
   int32_t gc_interval;    /* g: informational (the caller schedules trie_prune_compact)    */
   int32_t kv_dtype;       /* TRIE_F32 or TRIE_BF16 (also the dtype of Q, new K/V, output)  */
+  int32_t n_pages;        /* 0: dense pools; > 0: paged pools of n_pages 64-slot pages (below) */
 } trie_cfg;
+
+/*
+ * KV pool layouts (per layer; K and V alike).
+ *   dense  (n_pages == 0): [R][Hkv][capacity][D] -- slot n of request r, KV head h at row
+ *          (r * Hkv + h) * capacity + n.
+ *   paged  (n_pages  > 0; physical memory follows the live trie):
+ *          [n_pages][Hkv][64][D] -- slot n of request r at row (page * Hkv + h) * 64 + n % 64
+ *          with page = page_table[r][n / 64] (trie_arrays.page_table, [R][capacity / 64]
+ *          int32; capacity % 64 == 0).  Request r's prompt occupies the fixed pages
+ *          off_r .. off_r + ceil(t_r / 64) - 1, off_r = sum_{q < r} ceil(t_q / 64) (the
+ *          caller's prefill writes them); every other page sits in a device free queue.
+ *          trie_beam_step / trie_append take pages from it when N grows into a new 64-slot
+ *          block (TRIE_ST_CAPACITY latches when it is empty); trie_prune_compact returns
+ *          the pages above the compacted N (§3.5: pruned rows free their memory).
+ *          trie_arrays.page_ctr [4] uint32: pops, pushes, peak pages in use (since trie_create),
+ *          n_pages; pages
+ *          in use = n_pages - (pushes + free_at_create - pops) (see trie_page_stats).
+ *          Paged pools are supported by the handle's calls (trie_rope_kv_append,
+ *          trie_attn_decode_rope, trie_prune_compact); the handle-less trie_attn_decode
+ *          addresses dense pools only.
+ */
 
 typedef struct trie_handle trie_handle;
 
@@ -94,7 +116,24 @@ typedef struct trie_arrays {
   int32_t b_live; /* live beams: 1 before the first append, then b (host-tracked) */
   int32_t steps;  /* appends done since create/reset (host-tracked) */
   uint32_t* finished; /* [R][32]: beam j's last generated token is the EOS id (trie_set_eos) */
+  int32_t* page_table; /* paged pools: [R][capacity / 64] page of each 64-slot block (else NULL) */
+  uint32_t* page_ctr;  /* paged pools: [4] = pops, pushes, peak pages in use, n_pages */
 } trie_arrays;
+
+/*
+ * SURVEY §8(f) NEXT-3, sliding-window eviction (paged pools, cfg.window > 0; the paper
+ * evaluates SWA models, and keeps their whole cache): return to the free queue
+ * the page of every 64-slot block of each request that holds only prompt rows below
+ * min_j (depth[leaf_j] - W + 1) -- rows outside every live beam's window (reading R14) for
+ * the rest of the job, since leaf depths only grow.  Attention never reads them again and
+ * GC never moves prompt rows.  Contract: after trie_reset the prompt maps to its original
+ * pages again and the caller must re-write (prefill) their K/V before the first attention.
+ * Async on stream; EINVAL for dense pools or window == 0.
+ */
+int trie_swa_evict(trie_handle* h, cudaStream_t stream);
+
+/* Paged pools: host copy of {pages in use, peak pages in use, n_pages} (synchronises). */
+int trie_page_stats(trie_handle* h, int32_t* stats_host, cudaStream_t stream);
 
 /* Workspace bytes for a configuration (metadata + scratch of beam_step / prune). */
 int trie_workspace_bytes(const trie_cfg* cfg, size_t* bytes);

@@ -24,13 +24,14 @@ SYMBOLS = ["trie_workspace_bytes", "trie_create", "trie_reset", "trie_destroy", 
            "trie_append", "trie_prune_compact", "trie_read_hyps", "trie_status", "trie_last_error",
            "trie_version", "trie_launch_count", "trie_attn_decode_rope", "trie_attn_plan_info",
            "trie_batch_reorder_kv", "trie_set_eos", "trie_gather_setup", "trie_gather_wait",
-           "trie_ipc_alloc", "trie_ipc_open", "trie_ipc_close", "trie_ipc_free"]
+           "trie_ipc_alloc", "trie_ipc_open", "trie_ipc_close", "trie_ipc_free", "trie_page_stats",
+           "trie_swa_evict"]
 
 
 class trie_cfg(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "n_requests", "beam_width", "max_prompt_len", "capacity", "n_layers", "n_q_heads",
-        "n_kv_heads", "head_dim", "vocab", "window", "gc_interval", "kv_dtype")]
+        "n_kv_heads", "head_dim", "vocab", "window", "gc_interval", "kv_dtype", "n_pages")]
 
 
 class trie_arrays(ctypes.Structure):
@@ -38,7 +39,7 @@ class trie_arrays(ctypes.Structure):
                 ("beam_mask", ctypes.c_void_p), ("leaf", ctypes.c_void_p), ("score", ctypes.c_void_p),
                 ("n_nodes", ctypes.c_void_p), ("prompt_len", ctypes.c_void_p),
                 ("status", ctypes.c_void_p), ("b_live", ctypes.c_int32), ("steps", ctypes.c_int32),
-                ("finished", ctypes.c_void_p)]
+                ("finished", ctypes.c_void_p), ("page_table", ctypes.c_void_p), ("page_ctr", ctypes.c_void_p)]
 
 
 _lib = None
@@ -76,6 +77,8 @@ def load(path: str = LIB_PATH):
         "trie_launch_count": (ctypes.c_ulonglong, []),
         "trie_batch_reorder_kv": (ctypes.c_int, [I32] * 7 + [P] * 3 + [P] * 4 + [P, P]),
         "trie_set_eos": (ctypes.c_int, [P, I32]),
+        "trie_page_stats": (ctypes.c_int, [P, P, P]),
+        "trie_swa_evict": (ctypes.c_int, [P, P]),
         "trie_gather_setup": (ctypes.c_int, [P, I32, I32, P, P]),
         "trie_gather_wait": (ctypes.c_int, [P, P, P]),
         "trie_ipc_alloc": (ctypes.c_int, [SZ, ctypes.POINTER(P), P]),
@@ -115,8 +118,9 @@ def _stream(stream=None):
     return s.cuda_stream
 
 
-def make_cfg(R, b, t_max, capacity, L, Hq, Hkv, D, V, window=0, gc_interval=1, kv_dtype=TRIE_BF16):
-    return trie_cfg(R, b, t_max, capacity, L, Hq, Hkv, D, V, window, gc_interval, kv_dtype)
+def make_cfg(R, b, t_max, capacity, L, Hq, Hkv, D, V, window=0, gc_interval=1, kv_dtype=TRIE_BF16,
+             n_pages=0):
+    return trie_cfg(R, b, t_max, capacity, L, Hq, Hkv, D, V, window, gc_interval, kv_dtype, n_pages)
 
 
 # ---- entry points (same names as the C ABI) ------------------------------------------
@@ -300,3 +304,14 @@ def device_tensor(ptr: int, shape, dtype):
     ts = {torch.bfloat16: "<i2", torch.int32: "<i4", torch.float32: "<f4"}[dtype]
     t = torch.as_tensor(_CudaArray(ptr, shape, ts), device="cuda")
     return t.view(dtype) if dtype == torch.bfloat16 else t
+
+
+# ---- NEXT-2: paged pools -----------------------------------------------------------------
+def trie_page_stats(h, stream=None) -> dict:
+    st = (ctypes.c_int32 * 3)()
+    _check(load().trie_page_stats(h, ctypes.cast(st, ctypes.c_void_p), _stream(stream)), "trie_page_stats")
+    return dict(in_use=int(st[0]), peak=int(st[1]), n_pages=int(st[2]))
+
+
+def trie_swa_evict(h, stream=None):
+    _check(load().trie_swa_evict(h, _stream(stream)), "trie_swa_evict")

@@ -52,6 +52,9 @@ static int validate(const trie_cfg* c) {
   if (c->window < 0) return trie_set_error(TRIE_EINVAL, "window < 0");
   if (c->kv_dtype != TRIE_F32 && c->kv_dtype != TRIE_BF16)
     return trie_set_error(TRIE_EINVAL, "kv_dtype");
+  if (c->n_pages < 0) return trie_set_error(TRIE_EINVAL, "n_pages < 0");
+  if (c->n_pages > 0 && c->capacity % 64)
+    return trie_set_error(TRIE_EINVAL, "paged pools need capacity %% 64 == 0");
   return TRIE_OK;
 }
 
@@ -112,6 +115,13 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
   char* rtab = take(R * TRIE_MAX_BEAMS * (c->head_dim / 2) * 8);
   char* fin = take(R * TRIE_MAX_BEAMS * 4);
   char* gat = take(64);  // gather ticket + completed-launch counter (NEXT-4)
+  // paged pools (NEXT-2): page table, pages per request, prompt page base, free queue, counters
+  const size_t np = c->n_pages > 0 ? (size_t)c->n_pages : 0;
+  char* pt = take(np ? R * (cap / 64) * 4 : 0);
+  char* pused = take(np ? R * 4 : 0);
+  char* pbase = take(np ? R * 4 : 0);
+  char* fq = take(np * 4);
+  char* pctr = take(np ? 64 : 0);
   if (h) {
     h->token = (int32_t*)token;
     h->parent = (int32_t*)parent;
@@ -142,6 +152,11 @@ size_t trie_layout(const trie_cfg* c, trie_handle* h, char* base) {
     h->fin = (uint32_t*)fin;
     h->g_ticket = (uint32_t*)gat;
     h->g_epoch = (uint32_t*)gat + 1;
+    h->page_table = np ? (int32_t*)pt : nullptr;
+    h->pages_used = np ? (int32_t*)pused : nullptr;
+    h->page_base = np ? (int32_t*)pbase : nullptr;
+    h->free_q = np ? (int32_t*)fq : nullptr;
+    h->page_ctr = np ? (uint32_t*)pctr : nullptr;
     h->chunks = (int32_t)chunks;
   }
   return off;
@@ -188,14 +203,30 @@ int trie_create(const trie_cfg* cfg, void* workspace, size_t workspace_bytes,
   h->ws_bytes = workspace_bytes;
   trie_layout(cfg, h, (char*)workspace);
   h->host_tlen.assign(prompt_lens_host, prompt_lens_host + cfg->n_requests);
+  std::vector<int32_t> pbase(cfg->n_requests, 0);
+  if (cfg->n_pages > 0) {  // fixed prompt pages: request r from off_r = sum_{q<r} ceil(t_q/64)
+    int off = 0;
+    for (int r = 0; r < cfg->n_requests; ++r) {
+      pbase[r] = off;
+      off += (prompt_lens_host[r] + 63) / 64;
+    }
+    if (off > cfg->n_pages) {
+      delete h;
+      return trie_set_error(TRIE_ECAPACITY, "n_pages %d < %d prompt pages", cfg->n_pages, off);
+    }
+    h->prompt_pages = off;
+  }
   cudaError_t e = cudaMemcpyAsync(h->tlen, prompt_lens_host, cfg->n_requests * 4,
                                   cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess && cfg->n_pages > 0)
+    e = cudaMemcpyAsync(h->page_base, pbase.data(), cfg->n_requests * 4, cudaMemcpyHostToDevice, stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(h->prompts, prompt_tokens,
                         (size_t)cfg->n_requests * cfg->max_prompt_len * 4,
                         cudaMemcpyDeviceToDevice, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->status, 0, 4, stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->g_ticket, 0, 8, stream);  // ticket, epoch
+  if (e == cudaSuccess && h->page_ctr) e = cudaMemsetAsync(h->page_ctr, 0, 16, stream);
   if (e == cudaSuccess)
     e = cudaMemsetAsync(h->cnt_row, 0, (size_t)cfg->n_requests * (TRIE_MAX_BEAMS + 1) * 4, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // prompt_lens_host may be freed
@@ -227,6 +258,27 @@ int trie_destroy(trie_handle* h) {
   return TRIE_OK;
 }
 
+int trie_swa_evict(trie_handle* h, cudaStream_t stream) {
+  if (!h) return trie_set_error(TRIE_EINVAL, "null handle");
+  if (h->cfg.n_pages <= 0 || h->cfg.window <= 0)
+    return trie_set_error(TRIE_EINVAL, "trie_swa_evict: paged pools with a window only");
+  return trie::launch_swa_evict(h, stream);
+}
+
+int trie_page_stats(trie_handle* h, int32_t* stats_host, cudaStream_t stream) {
+  if (!h || !stats_host) return trie_set_error(TRIE_EINVAL, "null argument");
+  if (h->cfg.n_pages <= 0) return trie_set_error(TRIE_EINVAL, "dense pools: no pages");
+  uint32_t c[4];
+  cudaError_t e = cudaMemcpyAsync(c, h->page_ctr, 16, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return trie_set_error(TRIE_ECUDA, "trie_page_stats: %s", cudaGetErrorString(e));
+  const uint32_t free0 = (uint32_t)(h->cfg.n_pages - h->prompt_pages);
+  stats_host[0] = h->cfg.n_pages - (int32_t)(c[1] + free0 - c[0]);
+  stats_host[1] = (int32_t)c[2];
+  stats_host[2] = h->cfg.n_pages;
+  return TRIE_OK;
+}
+
 int trie_get_arrays(const trie_handle* h, trie_arrays* o) {
   if (!h || !o) return trie_set_error(TRIE_EINVAL, "null argument");
   o->token = h->token;
@@ -241,6 +293,8 @@ int trie_get_arrays(const trie_handle* h, trie_arrays* o) {
   o->b_live = h->b_live;
   o->steps = h->steps;
   o->finished = h->fin;
+  o->page_table = h->page_table;
+  o->page_ctr = h->page_ctr;
   return TRIE_OK;
 }
 
@@ -321,12 +375,34 @@ size_t trie_attn_scratch_bytes(const trie_cfg* cfg, int32_t b_live, int32_t rows
   return (a > b ? a : b) + 256;
 }
 
+// pt: the handle's page table for paged pools (NEXT-2), NULL for dense pools
+static int attn_decode_impl(const trie_cfg* cfg, int32_t b_live, const void* q, const void* k_pool,
+                            const void* v_pool, const int32_t* prompt_len, const int32_t* parent,
+                            const int32_t* depth, const int32_t* leaf_ids, const int32_t* n_nodes,
+                            const uint32_t* beam_mask, int32_t window, int32_t rows_hint, void* out,
+                            float* lse, void* scratch, size_t scratch_bytes, uint32_t* status,
+                            cudaStream_t stream, const int32_t* pt);
+
 int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const void* k_pool,
                      const void* v_pool, const int32_t* prompt_len, const int32_t* parent,
                      const int32_t* depth, const int32_t* leaf_ids, const int32_t* n_nodes,
                      const uint32_t* beam_mask, int32_t window, int32_t rows_hint, void* out,
                      float* lse, void* scratch, size_t scratch_bytes, uint32_t* status,
                      cudaStream_t stream) {
+  if (cfg && cfg->n_pages > 0)
+    return trie_set_error(TRIE_EINVAL, "trie_attn_decode addresses dense pools; paged pools go "
+                                       "through the handle (trie_attn_decode_rope)");
+  return attn_decode_impl(cfg, b_live, q, k_pool, v_pool, prompt_len, parent, depth, leaf_ids, n_nodes,
+                          beam_mask, window, rows_hint, out, lse, scratch, scratch_bytes, status, stream,
+                          nullptr);
+}
+
+static int attn_decode_impl(const trie_cfg* cfg, int32_t b_live, const void* q, const void* k_pool,
+                            const void* v_pool, const int32_t* prompt_len, const int32_t* parent,
+                            const int32_t* depth, const int32_t* leaf_ids, const int32_t* n_nodes,
+                            const uint32_t* beam_mask, int32_t window, int32_t rows_hint, void* out,
+                            float* lse, void* scratch, size_t scratch_bytes, uint32_t* status,
+                            cudaStream_t stream, const int32_t* pt) {
   int rc = validate(cfg);
   if (rc) return rc;
   if (b_live < 1 || b_live > cfg->beam_width) return trie_set_error(TRIE_EINVAL, "b_live");
@@ -363,6 +439,11 @@ int trie_attn_decode(const trie_cfg* cfg, int32_t b_live, const void* q, const v
   p.status = status;
   p.window = window;
   p.splits = pl.splits;
+  if (pt) {
+    p.pt = pt;
+    p.pt_stride = cfg->capacity / 64;
+    p.n_pages = cfg->n_pages;
+  }
   if (trie::attn_tc_supported(p))
     return trie::launch_attn_tc(p, stream);
   return trie::launch_attn_v1(p, stream);
@@ -418,6 +499,11 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
   p.k_new = k_new;
   p.v_new = v_new;
   p.rope_tab = h->rope_tab;
+  if (cfg->n_pages > 0) {  // paged pools (NEXT-2)
+    p.pt = h->page_table;
+    p.pt_stride = cfg->capacity / 64;
+    p.n_pages = cfg->n_pages;
+  }
   const bool fuse = trie::attn_rope_fusable(p) &&
                     (((uintptr_t)q | (uintptr_t)k_new | (uintptr_t)v_new) & 3) == 0;
   if (h->g_world > 1 && !fuse)
@@ -426,9 +512,9 @@ int trie_attn_decode_rope(trie_handle* h, const void* q, const void* k_new, cons
     int rc = trie::launch_rope_append(h, const_cast<void*>(q), const_cast<void*>(k_new), v_new,
                                       k_pool, v_pool, rope_theta, stream);
     if (rc) return rc;
-    return trie_attn_decode(cfg, b_live, q, k_pool, v_pool, h->tlen, h->parent, h->depth, h->leaf,
+    return attn_decode_impl(cfg, b_live, q, k_pool, v_pool, h->tlen, h->parent, h->depth, h->leaf,
                             h->n_nodes, h->mask, cfg->window, rows_hint, out, lse, scratch,
-                            scratch_bytes, h->status, stream);
+                            scratch_bytes, h->status, stream, h->page_table);
   }
   if (h->rope_tab_steps != h->steps || h->rope_tab_theta != rope_theta ||
       h->rope_tab_blive != b_live) {  // once per step, shared by all layers

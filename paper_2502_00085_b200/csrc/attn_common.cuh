@@ -53,7 +53,21 @@ struct AttnParams {
   // request whose b_live beams are all finished is done -- its CTAs read and write nothing
   const uint32_t* fin;
   GatherArgs ga;
+  // paged pools (cfg.n_pages > 0, NEXT-2): page table [R][pt_stride]; NULL = dense pools
+  const int32_t* pt;
+  int pt_stride;
+  int n_pages;
 };
+
+// Pool row of slot n of request r, KV head h (include/triedecode.h "KV pool layouts").
+__device__ __forceinline__ long attn_row(const AttnParams& p, int r, int h, int n) {
+  if (p.pt) return ((long)__ldg(p.pt + r * p.pt_stride + (n >> 6)) * p.Hkv + h) * 64 + (n & 63);
+  return ((long)r * p.Hkv + h) * p.cap + n;
+}
+// rows of the 2-D [rows][D] view of a pool
+inline long attn_pool_rows(const AttnParams& p) {
+  return p.pt ? (long)p.n_pages * p.Hkv * 64 : (long)p.R * p.Hkv * p.cap;
+}
 
 int launch_attn_v1(const AttnParams& p, cudaStream_t s);
 int launch_gather_wait(const GatherArgs& ga, int R, int b_live, int Hq, int D, void* dst, cudaStream_t s);

@@ -82,15 +82,16 @@ __global__ void __launch_bounds__(512) k_attn_v1(const AttnParams p) {
 #pragma unroll
     for (int c = 0; c < DC; ++c) acc[i][c] = 0.f;
   }
-  const T* kb = (const T*)p.k + ((size_t)r * p.Hkv + h) * p.cap * D;
-  const T* vb = (const T*)p.v + ((size_t)r * p.Hkv + h) * p.cap * D;
+  const T* kb = (const T*)p.k;
+  const T* vb = (const T*)p.v;
 
   for (int n0 = row_b; n0 < row_e; n0 += V1_TILE) {
     const int nt = min(V1_TILE, row_e - n0);
     for (int e = threadIdx.x; e < nt * D; e += blockDim.x) {
       const int n = e / D, d = e % D;
-      sK[n * Dp + d] = to_f(kb[(size_t)(n0 + n) * D + d]);
-      sV[n * D + d] = to_f(vb[(size_t)(n0 + n) * D + d]);
+      const size_t row = (size_t)attn_row(p, r, h, n0 + n);  // dense or paged (NEXT-2)
+      sK[n * Dp + d] = to_f(kb[row * D + d]);
+      sV[n * D + d] = to_f(vb[row * D + d]);
     }
     if (threadIdx.x < nt) {
       sMask[threadIdx.x] = p.mask[mbase + n0 + threadIdx.x];

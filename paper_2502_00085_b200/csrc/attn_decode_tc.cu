@@ -980,7 +980,7 @@ int launch_attn_tc(const AttnParams& p, cudaStream_t s) {
   const TcKernel* k = select_tc(p.D, p.b_live * (p.Hq / p.Hkv), p.rope != 0);
   if (!k) return trie_set_error(TRIE_EINVAL, "tensor-core attention: unsupported head_dim %d", p.D);
   CUtensorMap km, vm, kmh, vmh;
-  const long rows = (long)p.R * p.Hkv * p.cap;
+  const long rows = attn_pool_rows(p);
   int rc = cached_tensor_map(&km, p.k, p.D, rows);
   if (!rc) rc = cached_tensor_map(&vm, p.v, p.D, rows);
   if (!rc) rc = cached_tensor_map(&kmh, p.k, p.D, rows, TC_TR / 2);

@@ -232,7 +232,6 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
     if (lane == 0) {
       const bool isv = warp != 0;
       bool appended = !ROPE;
-      const int row_base = (r * p.Hkv + h) * p.cap;
       const size_t mbase = (size_t)r * p.cap;
       const int ns = isv ? STV : STK;
       uint64_t* fb = isv ? fullV : fullK;
@@ -248,12 +247,13 @@ __global__ void __launch_bounds__(UCfg<D, STK, STV>::THREADS) k_attn_umma(
           appended = true;
         }
         const int n0 = (it.tile0 + i) * TC_TR;
+        const int row = (int)attn_row(p, r, h, n0);
         // mask / depth words clamped to the [R][cap] arrays (cap % 4 == 0: 16-byte granules)
         const uint32_t mdb = isv ? (uint32_t)min(TC_TR, p.cap - n0) * 4u : 0u;
         mbar_expect_tx(&fb[s], C::TILE + 2 * mdb);
 #pragma unroll
         for (int bx = 0; bx < D / TC_CW; ++bx)
-          tma_load_2d(base + s * C::TILE + bx * TC_TR * 64, map, bx * TC_CW, row_base + n0, &fb[s]);
+          tma_load_2d(base + s * C::TILE + bx * TC_TR * 64, map, bx * TC_CW, row, &fb[s]);
         if (isv) {
           const uint32_t md = smem_u32(smem + C::OFF_MD + s * 512);
           bulk_load_1d(md, p.mask + mbase + n0, mdb, &fb[s]);
@@ -677,7 +677,7 @@ int launch_attn_umma(const AttnParams& p, cudaStream_t s) {
   const UKernel* k = select_u(p.D, p.rope != 0);
   if (!k) return trie_set_error(TRIE_EINVAL, "tcgen05 attention: unsupported head_dim %d", p.D);
   CUtensorMap km, vm;
-  const long rows = (long)p.R * p.Hkv * p.cap;
+  const long rows = attn_pool_rows(p);
   int rc = cached_tensor_map(&km, p.k, p.D, rows);
   if (!rc) rc = cached_tensor_map(&vm, p.v, p.D, rows);
   if (rc) return rc;

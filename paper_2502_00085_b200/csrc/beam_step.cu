@@ -185,13 +185,34 @@ __device__ __forceinline__ uint64_t row_key(float x, int v) {
   return ((uint64_t)f2ord(x) << 32) | (uint32_t)(~(uint32_t)v);
 }
 
+// ---- paged pools (NEXT-2): map pages until request r's table covers n_slots ----------
+// One thread per request.  Pops take free-queue entry ctr[0]; the queue is empty when that
+// entry has not been pushed yet (pushes happen only in k_page_release, another launch).
+__device__ void page_grow(const PageArgs& pg, int r, int cap, int n_slots, uint32_t* status) {
+  const int stride = cap / 64, need = (n_slots + 63) / 64;
+  const uint32_t nfree0 = (uint32_t)(pg.n_pages - pg.prompt_pages);
+  int used = pg.used[r];
+  while (used < need) {
+    const uint32_t i = atomicAdd(&pg.ctr[0], 1u);
+    const uint32_t pushes = *(volatile uint32_t*)&pg.ctr[1];
+    if (i >= nfree0 + pushes) {  // out of pages
+      latch(status, TRIE_ST_CAPACITY);
+      break;
+    }
+    pg.pt[r * stride + used] = pg.fq[i % (uint32_t)pg.n_pages];
+    ++used;
+    atomicMax(&pg.ctr[2], (uint32_t)pg.n_pages - (nfree0 + pushes - (i + 1u)));  // peak in use
+  }
+  pg.used[r] = used;
+}
+
 // ---- append (Alg. 2 l.10-11) -----------------------------------------------------------
 // Called by all threads of a CTA for request r with the selection in shared memory.
 __device__ void append_sel(int r, int b_new, int b_old, const int* sp, const int* st,
                            const float* ss, int32_t* token, int32_t* parent, int32_t* depth,
                            uint32_t* mask, int32_t* leaf, float* score, int32_t* nn,
                            int32_t* nkv, const int32_t* tlen, int cap, uint32_t* status,
-                           uint32_t* fin, int eos) {
+                           uint32_t* fin, int eos, const PageArgs& pg) {
   __shared__ int sm_old_leaf[TRIE_MAX_BEAMS];
   const size_t base = (size_t)r * cap;
   const int N = nn[r], t = tlen[r];
@@ -202,6 +223,7 @@ __device__ void append_sel(int r, int b_new, int b_old, const int* sp, const int
     if (threadIdx.x == 0) latch(status, TRIE_ST_CAPACITY);
     return;
   }
+  if (pg.n_pages > 0 && threadIdx.x == 0) page_grow(pg, r, cap, N + b_new, status);
   // update_mask over generated nodes: new bit r = old bit j_r
   for (int n = t + threadIdx.x; n < N; n += blockDim.x) {
     const uint32_t w = mask[base + n];
@@ -235,7 +257,8 @@ __device__ void append_sel(int r, int b_new, int b_old, const int* sp, const int
 __global__ void k_append(const int32_t* par, const int32_t* tok, const float* sc, int b_new,
                          int b_old, int32_t* token, int32_t* parent, int32_t* depth,
                          uint32_t* mask, int32_t* leaf, float* score, int32_t* nn, int32_t* nkv,
-                         const int32_t* tlen, int cap, uint32_t* status, uint32_t* fin, int eos) {
+                         const int32_t* tlen, int cap, uint32_t* status, uint32_t* fin, int eos,
+                         PageArgs pg) {
   __shared__ int sp[TRIE_MAX_BEAMS], st[TRIE_MAX_BEAMS];
   __shared__ float ss[TRIE_MAX_BEAMS];
   const int r = blockIdx.x;
@@ -246,7 +269,7 @@ __global__ void k_append(const int32_t* par, const int32_t* tok, const float* sc
   }
   __syncthreads();
   append_sel(r, b_new, b_old, sp, st, ss, token, parent, depth, mask, leaf, score, nn, nkv,
-             tlen, cap, status, fin, eos);
+             tlen, cap, status, fin, eos, pg);
 }
 
 // ---- the fused beam step ----------------------------------------------------------------
@@ -277,6 +300,7 @@ struct BeamStepArgs {
   // as one-hot at eos: lse 0, one candidate, score unchanged); eos < 0 disables.
   int eos;
   uint32_t* fin;  // [R][32]
+  PageArgs pg;    // paged pools (NEXT-2): pages mapped as N grows
 };
 
 // element index of item i of this thread within the row
@@ -535,7 +559,7 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
   }
   __syncthreads();
   append_sel(r, a.b, b_live, sp, st, ss, a.token, a.parent, a.depth, a.mask, a.leaf, a.score,
-             a.nn, a.nkv, a.tlen, a.cap, a.status, a.fin, a.eos);
+             a.nn, a.nkv, a.tlen, a.cap, a.status, a.fin, a.eos, a.pg);
 }
 
 // Register-path kernel: grid (chunks, rows), one item per CTA (any V; the TMA kernel
@@ -600,6 +624,7 @@ int launch_beam_step(trie_handle* h, const float* logits, int32_t* out_par, int3
   a.out_par = out_par; a.out_tok = out_tok; a.out_sc = out_sc;
   a.eos = h->eos;
   a.fin = h->fin;
+  a.pg = page_args(h);
   dim3 grid(a.chunks, c.n_requests * h->b_live);
   if (vec)
     launch_k(k_beam_step<true>, grid, dim3(BS), 0, s, a);
@@ -614,7 +639,7 @@ int launch_append(trie_handle* h, const int32_t* par, const int32_t* tok, const 
   k_append<<<c.n_requests, 256, 0, s>>>(par, tok, sc, c.beam_width, h->b_live, h->token,
                                         h->parent, h->depth, h->mask, h->leaf, h->score,
                                         h->n_nodes, h->n_kv, h->tlen, c.capacity, h->status, h->fin,
-                                        h->eos);
+                                        h->eos, page_args(h));
   return trie_check_launch("k_append");
 }
 

@@ -53,6 +53,13 @@ struct trie_handle {
   uint32_t* g_flags[8] = {};
   uint32_t* g_ticket = nullptr;
   uint32_t* g_epoch = nullptr;
+  // paged pools (cfg.n_pages > 0, NEXT-2)
+  int32_t* page_table = nullptr;  // [R][cap/64]
+  int32_t* pages_used = nullptr;  // [R] pages mapped (blocks [0, used) of the table)
+  int32_t* page_base = nullptr;   // [R] first prompt page (fixed)
+  int32_t* free_q = nullptr;      // [n_pages] ring of free pages
+  uint32_t* page_ctr = nullptr;   // [0] pops, [1] pushes, [2] peak in use, [3] n_pages
+  int32_t prompt_pages = 0;       // host: sum over requests of ceil(t_r / 64)
   // host-tracked state
   int32_t b_live = 1;
   int32_t steps = 0;
@@ -79,6 +86,29 @@ inline trie::GatherArgs trie_gather_args(const trie_handle* h) {
   return ga;
 }
 
+// Paged pools (NEXT-2): the kernels' view of the page state.  Free queue: logical entry i
+// lives at fq[i % n_pages]; entries [0, n_pages - prompt_pages) are filled by k_init, pushes
+// append at n_pages - prompt_pages + ctr[1], pops take entry ctr[0].
+struct PageArgs {
+  int32_t* pt;          // [R][cap/64]
+  int32_t* used;        // [R]
+  const int32_t* base;  // [R]
+  int32_t* fq;          // [n_pages]
+  uint32_t* ctr;        // [4] pops, pushes, peak in use, n_pages
+  int n_pages, prompt_pages;
+};
+inline PageArgs page_args(const trie_handle* h) {
+  PageArgs a = {};
+  a.n_pages = h->cfg.n_pages > 0 ? h->cfg.n_pages : 0;
+  a.pt = h->page_table;
+  a.used = h->pages_used;
+  a.base = h->page_base;
+  a.fq = h->free_q;
+  a.ctr = h->page_ctr;
+  a.prompt_pages = h->prompt_pages;
+  return a;
+}
+
 // carve the workspace; with h == nullptr only computes the size
 size_t trie_layout(const trie_cfg* cfg, trie_handle* h, char* base);
 
@@ -90,6 +120,7 @@ int launch_append(trie_handle* h, const int32_t* par, const int32_t* tok, const 
 int launch_beam_step(trie_handle* h, const float* logits, int32_t* out_par, int32_t* out_tok,
                      float* out_sc, cudaStream_t s);
 int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t s);
+int launch_swa_evict(trie_handle* h, cudaStream_t s);
 int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, void* kpool,
                        void* vpool, float theta, cudaStream_t s);
 int launch_read_hyps(trie_handle* h, int32_t max_len, int32_t* out_dev, cudaStream_t s);

@@ -57,7 +57,7 @@ template <typename T>
 __global__ void __launch_bounds__(ROPE_BS) k_rope_append(
     T* __restrict__ q, T* __restrict__ k_new, const T* __restrict__ v_new, T* __restrict__ kpool,
     T* __restrict__ vpool, const int32_t* __restrict__ leaf, const float2* __restrict__ tab,
-    int b_live, int Hq, int Hkv, int D, int cap) {
+    int b_live, int Hq, int Hkv, int D, int cap, const int32_t* __restrict__ pt) {
   constexpr int VN = Vec16<T>::N;
   __shared__ float s_cos[128], s_sin[128];  // D <= 256
   pdl_trigger();
@@ -66,6 +66,11 @@ __global__ void __launch_bounds__(ROPE_BS) k_rope_append(
   const int r = rj / b_live;
   const int slot = leaf[r * TRIE_MAX_BEAMS + rj % b_live];
   const int half = D / 2;
+  // pool row of (r, KV head hh, slot): dense [R][Hkv][cap][D] or paged (NEXT-2)
+  auto prow = [&](int hh) -> size_t {
+    return pt ? ((size_t)pt[r * (cap / 64) + (slot >> 6)] * Hkv + hh) * 64 + (slot & 63)
+              : ((size_t)r * Hkv + hh) * cap + slot;
+  };
   for (int i = threadIdx.x; i < half; i += ROPE_BS) {  // the step's table (k_rope_table)
     const float2 c = tab[(size_t)rj * half + i];
     s_cos[i] = c.x;
@@ -110,14 +115,14 @@ __global__ void __launch_bounds__(ROPE_BS) k_rope_append(
         *reinterpret_cast<int4*>(e + c * VN) = o1;
         *reinterpret_cast<int4*>(e + half + c * VN) = o2;
         if (hh >= Hq) {
-          T* dst = kpool + (((size_t)r * Hkv + (hh - Hq)) * cap + slot) * D;
+          T* dst = kpool + prow(hh - Hq) * D;
           *reinterpret_cast<int4*>(dst + c * VN) = o1;
           *reinterpret_cast<int4*>(dst + half + c * VN) = o2;
         }
       } else if (it < total) {
         const int e = (it - n_rot) * VN;
         const int hh = e / D, d = e % D;
-        *reinterpret_cast<int4*>(vpool + (((size_t)r * Hkv + hh) * cap + slot) * D + d) = lo[u];
+        *reinterpret_cast<int4*>(vpool + prow(hh) * D + d) = lo[u];
       }
     }
   }
@@ -168,12 +173,12 @@ int launch_rope_append(trie_handle* h, void* q, void* k_new, const void* v_new, 
              (__nv_bfloat16*)q, (__nv_bfloat16*)k_new, (const __nv_bfloat16*)v_new,
              (__nv_bfloat16*)kpool, (__nv_bfloat16*)vpool, (const int32_t*)h->leaf,
              (const float2*)h->rope_tab, h->b_live, c.n_q_heads, c.n_kv_heads, c.head_dim,
-             c.capacity);
+             c.capacity, (const int32_t*)h->page_table);
   } else {
     launch_k(k_rope_append<float>, grid, dim3(ROPE_BS), 0, s, (float*)q, (float*)k_new,
              (const float*)v_new, (float*)kpool, (float*)vpool, (const int32_t*)h->leaf,
              (const float2*)h->rope_tab, h->b_live, c.n_q_heads, c.n_kv_heads, c.head_dim,
-             c.capacity);
+             c.capacity, (const int32_t*)h->page_table);
   }
   return trie_check_launch("k_rope_append");
 }

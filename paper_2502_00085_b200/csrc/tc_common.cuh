@@ -198,7 +198,7 @@ __device__ __forceinline__ void append_leaves_rope_work(const AttnParams& p, int
     const int slot = first_leaf + j;
     if (slot < slot_lo || slot >= slot_hi) continue;
     const size_t rj = (size_t)r * p.b_live + j;
-    __nv_bfloat16* dst = (e < nk ? kpool : vpool) + (((size_t)r * p.Hkv + h) * p.cap + slot) * D;
+    __nv_bfloat16* dst = (e < nk ? kpool : vpool) + (size_t)attn_row(p, r, h, slot) * D;
     if (e < nk) {
       const int c = (e % CH) * 8;
       const __nv_bfloat16* src = kn + (rj * p.Hkv + h) * D;
@@ -248,15 +248,15 @@ __device__ __forceinline__ void prefetch_prompt_tiles(const CUtensorMap* kmap,
                                                       const AttnParams& p, int r, int h,
                                                       uint8_t* ring, uint64_t* full, int n) {
   using RG = Ring<D, STAGES>;
-  const int row_base = (r * p.Hkv + h) * p.cap;
   for (int i = 0; i < n; ++i) {
     const uint32_t st = smem_u32(ring + i * RG::STAGE_BYTES);
+    // prompt tiles: their pages (paged pools) are fixed at trie_create
+    const int row = (int)attn_row(p, r, h, i * TC_TR);
     mbar_expect_tx(&full[i], 2 * RG::TILE_BYTES);
 #pragma unroll
     for (int bx = 0; bx < D / TC_CW; ++bx) {
-      tma_load_2d(st + bx * TC_TR * 64, kmap, bx * TC_CW, row_base + i * TC_TR, &full[i]);
-      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vmap, bx * TC_CW, row_base + i * TC_TR,
-                  &full[i]);
+      tma_load_2d(st + bx * TC_TR * 64, kmap, bx * TC_CW, row, &full[i]);
+      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vmap, bx * TC_CW, row, &full[i]);
     }
   }
 }
@@ -275,7 +275,6 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
   // an earlier tile -- hence only stages already used, i >= STAGES -- and those rows are
   // masked, n >= N): the 64-row tile granularity over-fetched ~half a tile per item.
   using RG = Ring<D, STAGES>;
-  const int row_base = (r * p.Hkv + h) * p.cap;
   const size_t mbase = (size_t)r * p.cap;
   bool appended = app_done == nullptr;
   for (int i = i_begin; i < min(it.ntiles, i_end); ++i) {
@@ -291,6 +290,7 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
     }
     const uint32_t st = smem_u32(ring + s * RG::STAGE_BYTES);
     const int n0 = (it.tile0 + i) * TC_TR;
+    const int row = (int)attn_row(p, r, h, n0);
     // mask / depth words clamped to the [R][cap] arrays (cap % 4 == 0: 16-byte granules)
     const uint32_t mdb = (uint32_t)min(TC_TR, p.cap - n0) * 4u;
     const bool half = kmh != nullptr && i >= STAGES && it.N - n0 <= TC_TR / 2;
@@ -299,8 +299,8 @@ __device__ __forceinline__ void producer_loop(const CUtensorMap* kmap, const CUt
     const CUtensorMap* vm = half ? vmh : vmap;
 #pragma unroll
     for (int bx = 0; bx < D / TC_CW; ++bx) {
-      tma_load_2d(st + bx * TC_TR * 64, km, bx * TC_CW, row_base + n0, &full[s]);
-      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vm, bx * TC_CW, row_base + n0, &full[s]);
+      tma_load_2d(st + bx * TC_TR * 64, km, bx * TC_CW, row, &full[s]);
+      tma_load_2d(st + RG::TILE_BYTES + bx * TC_TR * 64, vm, bx * TC_CW, row, &full[s]);
     }
     bulk_load_1d(st + 2 * RG::TILE_BYTES, p.mask + mbase + n0, mdb, &full[s]);
     bulk_load_1d(st + 2 * RG::TILE_BYTES + TC_TR * 4, p.depth + mbase + n0, mdb, &full[s]);

@@ -37,13 +37,31 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total, int* sm_warp) 
 }
 
 // ---- Alg. 2 l.1 initialize_trie(prompt) --------------------------------------------------
+// Paged pools (NEXT-2): request r's prompt keeps its fixed pages page_base[r] + i; every
+// other page goes into the free queue (pages prompt_pages .. n_pages - 1, in order); the
+// counters restart (pops 0, pushes 0, peak = the prompt pages).
+
 __global__ void k_init(int32_t* token, int32_t* parent, int32_t* depth, uint32_t* mask,
                        int32_t* leaf, float* score, int32_t* nn, int32_t* nkv,
                        const int32_t* tlen, const int32_t* prompts, int t_max, int cap,
-                       uint32_t* fin) {
+                       uint32_t* fin, PageArgs pg) {
   const int r = blockIdx.x;
   const int t = tlen[r];
   const size_t base = (size_t)r * cap;
+  if (pg.n_pages > 0) {
+    const int np = (t + 63) / 64, stride = cap / 64;
+    for (int i = threadIdx.x; i < stride; i += blockDim.x) pg.pt[r * stride + i] = i < np ? pg.base[r] + i : -1;
+    if (threadIdx.x == 0) pg.used[r] = np;
+    const int nfree = pg.n_pages - pg.prompt_pages;
+    for (int i = r * blockDim.x + threadIdx.x; i < nfree; i += gridDim.x * blockDim.x)
+      pg.fq[i] = pg.prompt_pages + i;
+    if (r == 0 && threadIdx.x == 0) {
+      pg.ctr[0] = 0u;
+      pg.ctr[1] = 0u;
+      pg.ctr[2] = max(pg.ctr[2], (uint32_t)pg.prompt_pages);  // peak since trie_create
+      pg.ctr[3] = (uint32_t)pg.n_pages;
+    }
+  }
   for (int i = threadIdx.x; i < t; i += blockDim.x) {
     token[base + i] = prompts[(size_t)r * t_max + i];
     parent[base + i] = i - 1;
@@ -59,11 +77,12 @@ __global__ void k_init(int32_t* token, int32_t* parent, int32_t* depth, uint32_t
   }
 }
 
+
 int launch_init(trie_handle* h, cudaStream_t s) {
   const trie_cfg& c = h->cfg;
   k_init<<<c.n_requests, 256, 0, s>>>(h->token, h->parent, h->depth, h->mask, h->leaf, h->score,
                                       h->n_nodes, h->n_kv, h->tlen, h->prompts,
-                                      c.max_prompt_len, c.capacity, h->fin);
+                                      c.max_prompt_len, c.capacity, h->fin, page_args(h));
   return trie_check_launch("k_init");
 }
 
@@ -166,7 +185,8 @@ __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant
                                                            const int32_t* moves,
                                                            const int32_t* moves_dst,
                                                            const int32_t* n_moves, int Hkv,
-                                                           int hg, int row_bytes, int cap) {
+                                                           int hg, int row_bytes, int cap,
+                                                           const int32_t* __restrict__ pt) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, layer = blockIdx.y, h0 = blockIdx.z * hg;
@@ -196,6 +216,15 @@ __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant
         rem -= kv * nh * vpr;
         const int hh = rem / vpr, c = rem % vpr;
         const int src = moves[base + mi], dst = moves_dst[base + mi];
+        if (pt) {  // paged pools (NEXT-2): rows (page * Hkv + h) * 64 + slot % 64
+          char* pool = (char*)(kv ? pp.v[layer] : pp.k[layer]);
+          const int* ptr = pt + r * (cap / 64);
+          const size_t rs = ((size_t)ptr[src >> 6] * Hkv + h0 + hh) * 64 + (src & 63);
+          const size_t rd = ((size_t)ptr[dst >> 6] * Hkv + h0 + hh) * 64 + (dst & 63);
+          val[u] = *(const int4*)(pool + rs * row_bytes + (size_t)c * 16);
+          dstp[u] = pool + rd * row_bytes + (size_t)c * 16;
+          continue;
+        }
         char* pool = (kv ? vb : kb) + (size_t)hh * hstride;
         val[u] = *(const int4*)(pool + (size_t)src * row_bytes + (size_t)c * 16);
         dstp[u] = pool + (size_t)dst * row_bytes + (size_t)c * 16;
@@ -209,6 +238,58 @@ __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant
   }
 }
 
+// Paged pools (NEXT-2): after the compaction's K/V moves, the pages above each request's
+// new N go back to the free queue (a separate launch: the moves read those pages).
+__global__ void k_page_release(PageArgs pg, const int32_t* nn, int R, int cap) {
+  pdl_trigger();
+  pdl_wait();
+  const int stride = cap / 64;
+  const uint32_t nfree0 = (uint32_t)(pg.n_pages - pg.prompt_pages);
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+    const int keep = (nn[r] + 63) / 64, used = pg.used[r];
+    for (int i = keep; i < used; ++i) {
+      const uint32_t k = atomicAdd(&pg.ctr[1], 1u);
+      pg.fq[(nfree0 + k) % (uint32_t)pg.n_pages] = pg.pt[r * stride + i];
+      pg.pt[r * stride + i] = -1;
+    }
+    if (used > keep) pg.used[r] = keep;
+  }
+}
+
+// SURVEY §8(f) NEXT-3, SWA eviction (paged pools, window W > 0): every 64-slot block of
+// request r made only of prompt rows below min over the live leaves of
+// (depth[leaf] - W + 1) is outside every beam's window (reading R14) for the rest of the
+// job -- leaf depths only grow -- so its page goes back to the free queue.  The attention
+// kernels start at the window's first slot and never read such a block; prompt rows never
+// move (GC compacts generated rows only), so no later compaction touches it.
+__global__ void k_swa_evict(PageArgs pg, const int32_t* depth, const int32_t* leaf,
+                            const int32_t* tlen, int b_live, int window, int cap) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x, lane = threadIdx.x;
+  const size_t base = (size_t)r * cap;
+  const int lo = lane < b_live ? depth[base + leaf[r * TRIE_MAX_BEAMS + lane]] - window + 1 : INT_MAX;
+  const int lo_dep = __reduce_min_sync(0xffffffffu, lo);
+  if (lane != 0) return;
+  const int t = tlen[r], stride = cap / 64;
+  const int nblk = min(lo_dep, t) / 64;  // prompt rows have depth == slot (Alg. 2 l.1)
+  const uint32_t nfree0 = (uint32_t)(pg.n_pages - pg.prompt_pages);
+  for (int i = 0; i < nblk; ++i) {
+    const int pgid = pg.pt[r * stride + i];
+    if (pgid < 0) continue;  // evicted by an earlier step
+    const uint32_t k = atomicAdd(&pg.ctr[1], 1u);
+    pg.fq[(nfree0 + k) % (uint32_t)pg.n_pages] = pgid;
+    pg.pt[r * stride + i] = -1;
+  }
+}
+
+int launch_swa_evict(trie_handle* h, cudaStream_t s) {
+  const trie_cfg& c = h->cfg;
+  launch_k(k_swa_evict, dim3(c.n_requests), dim3(32), 0, s, page_args(h), (const int32_t*)h->depth,
+           (const int32_t*)h->leaf, (const int32_t*)h->tlen, h->b_live, c.window, c.capacity);
+  return trie_check_launch("k_swa_evict");
+}
+
 int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t s) {
   const trie_cfg& c = h->cfg;
   launch_k(k_prune_scan, dim3(c.n_requests), dim3(PRUNE_BS), 0, s, h->token, h->parent, h->depth,
@@ -216,7 +297,13 @@ int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t 
            h->moves, h->moves_dst, h->n_moves, h->b_live, c.capacity, h->status);
   int rc = trie_check_launch("k_prune_scan");
   if (rc) return rc;
-  if (c.n_layers == 0 || kp == nullptr) return TRIE_OK;
+  auto release = [&]() -> int {
+    if (c.n_pages <= 0) return TRIE_OK;
+    launch_k(k_page_release, dim3((c.n_requests + 127) / 128), dim3(128), 0, s, page_args(h),
+             (const int32_t*)h->n_nodes, c.n_requests, c.capacity);
+    return trie_check_launch("k_page_release");
+  };
+  if (c.n_layers == 0 || kp == nullptr) return release();
   PoolPtrs pp;
   for (int l = 0; l < c.n_layers; ++l) {
     pp.k[l] = kp[l];
@@ -230,8 +317,10 @@ int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t 
   dim3 grid(c.n_requests, c.n_layers, (c.n_kv_heads + hg - 1) / hg);
   launch_k(k_kv_compact, grid, dim3(COMPACT_BS), 0, s, pp, (const int32_t*)h->moves,
            (const int32_t*)h->moves_dst, (const int32_t*)h->n_moves, c.n_kv_heads, hg,
-           c.head_dim * esz, c.capacity);
-  return trie_check_launch("k_kv_compact");
+           c.head_dim * esz, c.capacity, (const int32_t*)h->page_table);
+  rc = trie_check_launch("k_kv_compact");
+  if (rc) return rc;
+  return release();
 }
 
 // ---- Alg. 2 l.14: hypotheses = root-to-leaf token paths ---------------------------------

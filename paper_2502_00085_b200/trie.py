@@ -13,13 +13,14 @@ from . import _lib as L
 
 class TrieState:
     def __init__(self, R, b, t_max, capacity, n_layers, Hq, Hkv, D, V, prompt_tokens, prompt_lens,
-                 window=0, gc_interval=1, dtype=torch.bfloat16, device="cuda", stream=None):
+                 window=0, gc_interval=1, dtype=torch.bfloat16, device="cuda", stream=None, n_pages=0):
         if not torch.cuda.is_available():
             raise L.TrieError("no CUDA device: libtriedecode has no CPU path")
         self.kv_dtype = L.TRIE_BF16 if dtype == torch.bfloat16 else L.TRIE_F32
         self.dtype = dtype
         self.cfg = L.make_cfg(R, b, t_max, capacity, n_layers, Hq, Hkv, D, V, window, gc_interval,
-                              self.kv_dtype)
+                              self.kv_dtype, n_pages)
+        self.n_pages = n_pages
         self.R, self.b, self.t_max, self.cap = R, b, t_max, capacity
         self.L, self.Hq, self.Hkv, self.D, self.V, self.window = n_layers, Hq, Hkv, D, V, window
         self.device = device
@@ -52,6 +53,8 @@ class TrieState:
         self.prompt_len = view(a.prompt_len, R, torch.int32, (R,))
         self.finished = view(a.finished, R * 32, torch.int32, (R, 32))  # uint32 flags
         self.status_word = view(a.status, 1, torch.int32, (1,))         # TRIE_ST_* bits
+        self.page_table = (view(a.page_table, R * (cap // 64), torch.int32, (R, cap // 64))
+                           if self.n_pages else None)                   # NEXT-2 paged pools
 
     @property
     def b_live(self) -> int:
@@ -62,10 +65,57 @@ class TrieState:
         return L.trie_get_arrays(self.h).steps
 
     def new_pools(self):
-        """Zero-initialised K and V pools, one [R][Hkv][cap][D] tensor per layer."""
-        shape = (self.L, self.R, self.Hkv, self.cap, self.D)
+        """Zero-initialised K and V pools, one tensor per layer: dense [R][Hkv][cap][D], or
+        paged [n_pages][Hkv][64][D] (include/triedecode.h "KV pool layouts")."""
+        shape = ((self.L, self.n_pages, self.Hkv, 64, self.D) if self.n_pages
+                 else (self.L, self.R, self.Hkv, self.cap, self.D))
         return (torch.zeros(shape, dtype=self.dtype, device=self.device),
                 torch.zeros(shape, dtype=self.dtype, device=self.device))
+
+    # ---- paged pools (NEXT-2): host-side views for prefill and tests (plain indexing) ----
+    def prompt_pages(self, r):
+        """Fixed pages of request r's prompt (off_r .. off_r + ceil(t_r / 64) - 1)."""
+        lens = self.prompt_len.cpu().tolist()
+        off = sum((int(t) + 63) // 64 for t in lens[:r])
+        return list(range(off, off + (int(lens[r]) + 63) // 64))
+
+    def write_rows(self, pool_l, rows):
+        """Write dense rows [R][Hkv][n][D] (slots 0..n-1 of every request) into a layer's
+        pool, through the page table when paged (the caller's prefill)."""
+        n = rows.shape[2]
+        if not self.n_pages:
+            pool_l[:, :, :n] = rows
+            return
+        pt = self.page_table.cpu()
+        for r in range(self.R):
+            for blk in range((n + 63) // 64):
+                if int(pt[r, blk]) < 0:  # block not mapped (beyond the request's N)
+                    continue
+                m = min(64, n - blk * 64)
+                pool_l[int(pt[r, blk]), :, :m] = rows[r, :, blk * 64: blk * 64 + m]
+
+    def dense_view(self, pool_l, n=None):
+        """[R][Hkv][n][D] copy of a layer's pool in slot order (tests)."""
+        n = self.cap if n is None else n
+        if not self.n_pages:
+            return pool_l[:, :, :n].clone()
+        pt = self.page_table.cpu()
+        out = torch.zeros(self.R, self.Hkv, n, self.D, dtype=pool_l.dtype, device=pool_l.device)
+        for r in range(self.R):
+            for blk in range((n + 63) // 64):
+                pg = int(pt[r, blk])
+                if pg < 0:
+                    continue
+                m = min(64, n - blk * 64)
+                out[r, :, blk * 64: blk * 64 + m] = pool_l[pg, :, :m]
+        return out
+
+    def swa_evict(self, stream=None):
+        """NEXT-3: free the pages of prompt blocks below every live beam's window."""
+        L.trie_swa_evict(self.h, stream)
+
+    def page_stats(self, stream=None) -> dict:
+        return L.trie_page_stats(self.h, stream)
 
     # ---- C ABI calls ----------------------------------------------------------------
     def set_eos(self, eos_id: int):

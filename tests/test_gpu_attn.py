@@ -118,6 +118,32 @@ def test_rope_kv_append_matches_oracle(dt):
 
 
 @pytest.mark.parametrize("name,R,b,t_max,Hq,Hkv,D,W", [
+    ("paged-narrow", 3, 4, 300, 8, 8, 96, 0),
+    ("paged-gqa-swa", 2, 4, 200, 8, 2, 128, 60),
+    ("paged-wide", 2, 8, 150, 32, 8, 128, 0),
+    ("paged-umma", 2, 16, 400, 8, 2, 128, 0),
+    ("paged-split", 1, 2, 1500, 2, 2, 128, 0),
+])
+def test_fused_paged_pools_match_oracle(name, R, b, t_max, Hq, Hkv, D, W):
+    """the same fused RoPE + append + attention over PAGED pools
+    ([n_pages][Hkv][64][D], 64-slot pages mapped through the page table as N grows,
+    returned by GC) -- identical results to the oracle as with dense pools."""
+    _fused_case(name, R, b, t_max, Hq, Hkv, D, W, paged=True)
+
+
+@pytest.mark.parametrize("name,R,b,t_max,Hq,Hkv,D,W,steps", [
+    ("evict-narrow", 2, 4, 300, 8, 2, 128, 100, 8),
+    ("evict-umma", 2, 16, 600, 8, 2, 128, 200, 6),
+    ("evict-d64", 1, 4, 500, 4, 1, 64, 64, 10),
+])
+def test_swa_eviction_frees_prompt_pages_and_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W, steps):
+    """with paged pools and a window, trie_swa_evict returns the pages
+    of prompt blocks below every live beam's window to the free queue (later appends reuse
+    them); attention over the remaining pages still equals the oracle (reading R14)."""
+    _fused_case(name, R, b, t_max, Hq, Hkv, D, W, steps=steps, paged=True, evict=True)
+
+
+@pytest.mark.parametrize("name,R,b,t_max,Hq,Hkv,D,W", [
     ("phi-fused", 2, 4, 300, 8, 8, 96, 0),
     ("gqa-fused", 2, 4, 200, 8, 2, 128, 0),
     ("swa-fused", 1, 4, 150, 4, 1, 64, 40),
@@ -146,7 +172,8 @@ def test_fused_ragged_matches_oracle(name, R, b, t_max, Hq, Hkv, D):
     _fused_case(name, R, b, t_max, Hq, Hkv, D, 0, ragged=True)
 
 
-def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False, steps=6, rho=0.5):
+def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False, steps=6, rho=0.5, paged=False,
+                evict=False):
     need_gpu()
     from paper_2502_00085_b200.trie import TrieState
     seed = zlib.crc32(name.encode()) % 1000
@@ -155,18 +182,27 @@ def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False, steps=6, rho=0.5
     prompts, lens = synth.prompts(seed, R, t_max, V, lens)
     sels = per_request_selections(seed, R, steps, b, V, rho)
     cap = (t_max + b * steps + b + 63) // 64 * 64
-    st = TrieState(R, b, t_max, cap, 1, Hq, Hkv, D, V, prompts, lens, window=W, dtype=torch.bfloat16)
+    st = TrieState(R, b, t_max, cap, 1, Hq, Hkv, D, V, prompts, lens, window=W, dtype=torch.bfloat16,
+                   n_pages=R * cap // 64 if paged else 0)
     kp, vp = st.new_pools()
     for par, tok in sels:
         st.append(torch.as_tensor(par, device="cuda"), torch.as_tensor(tok, device="cuda"))
         st.prune_compact(kp, vp)
+        if evict:  # NEXT-3: free the prompt pages below every live beam's window
+            st.swa_evict()
     tries = build_tries(prompts, lens, sels, b, g=1, final_gc=True)
+    if evict:  # every block of prompt rows below min_j (depth[leaf_j] - W + 1) is unmapped
+        pt = st.page_table.cpu().numpy()
+        for r, T in enumerate(tries):
+            lo = min(T.depth[x] for x in T.leaves) - W + 1
+            nblk = min(lo, T.t) // 64
+            assert nblk > 0 and np.all(pt[r, :nblk] == -1) and np.all(pt[r, nblk:(T.N + 63) // 64] >= 0)
     K = synth.normal(seed, 1, (R, Hkv, cap, D))
     Vv = synth.normal(seed, 2, (R, Hkv, cap, D))
     tK = torch.as_tensor(K, dtype=torch.float32).to(torch.bfloat16).cuda()
     tV = torch.as_tensor(Vv, dtype=torch.float32).to(torch.bfloat16).cuda()
-    kp[0].copy_(tK)
-    vp[0].copy_(tV)
+    st.write_rows(kp[0], tK)  # dense copy, or through the page table (NEXT-2)
+    st.write_rows(vp[0], tV)
     q = torch.as_tensor(synth.normal(seed, 3, (R, b, Hq, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
     kn = torch.as_tensor(synth.normal(seed, 4, (R, b, Hkv, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
     vn = torch.as_tensor(synth.normal(seed, 5, (R, b, Hkv, D)), dtype=torch.float32).to(torch.bfloat16).cuda()
@@ -178,8 +214,8 @@ def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False, steps=6, rho=0.5
     torch.cuda.synchronize()
     assert st.status() == 0
     o, l = out.float().cpu().numpy(), lse.cpu().numpy()
-    kpool_after = kp[0].float().cpu().numpy()
-    vpool_after = vp[0].float().cpu().numpy()
+    kpool_after = st.dense_view(kp[0]).float().cpu().numpy()
+    vpool_after = st.dense_view(vp[0]).float().cpu().numpy()
     for r in range(R):
         T = tries[r]
         Kr, Vr = Kh[r].copy(), Vh[r].copy()
@@ -340,11 +376,13 @@ def test_leaf_latch_and_reset_clears_status():
     from paper_2502_00085_b200.trie import TrieState
     prompts, lens = synth.prompts(5, 1, 6, 50)
     st = TrieState(1, 3, 6, 40, 0, 1, 1, 16, 50, prompts, lens, dtype=torch.float32)
-    st.beam_step(torch.randn(1, 1, 50, device="cuda"))
+    lg1 = torch.zeros(1, 1, 50, device="cuda")
+    lg1[0, 0, :3] = 10.0  # three equal-score beams
+    st.beam_step(lg1)
     assert st.status() == 0
     st.leaf[0, 1] = 9999
-    lg = torch.randn(1, 3, 50, device="cuda")
-    lg[0, 1] += 100.0  # every new beam's parent is the corrupted beam 1
+    lg = torch.zeros(1, 3, 50, device="cuda")
+    lg[0, 1, 5] = 50.0  # beam 1's continuation (log-prob ~0) outranks the flat rows (-log 50)
     st.beam_step(lg)
     assert st.status() & _lib.TRIE_ST_LEAF
     st.reset()

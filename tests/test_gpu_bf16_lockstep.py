@@ -43,9 +43,14 @@ def _bf16_np(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
+@pytest.mark.parametrize("paged", [False, True], ids=["dense", "paged"])
 @pytest.mark.parametrize("name,D,Hq,Hkv,b,R,t_max,s,W,paths", CASES)
-def test_bf16_lockstep_decode(name, D, Hq, Hkv, b, R, t_max, s, W, paths):
+def test_bf16_lockstep_decode(name, D, Hq, Hkv, b, R, t_max, s, W, paths, paged):
+    """paged: the same decode over paged pools (pages mapped as the
+    trie grows, returned by GC)."""
     need_gpu()
+    if paged and name not in ("narrow-gqa", "wide-swa", "tcgen05"):
+        pytest.skip("paged pools: a subset of the shapes")
     from paper_2502_00085_b200 import _lib
     from paper_2502_00085_b200.model import TinyModel
     from paper_2502_00085_b200.trie import TrieState
@@ -56,16 +61,25 @@ def test_bf16_lockstep_decode(name, D, Hq, Hkv, b, R, t_max, s, W, paths):
     gm = TinyModel(seed, L=L, d=Hq * D, Hq=Hq, Hkv=Hkv, D=D, ffn=ffn, V=V, rope_base=base,
                    kappa=4.0, dtype=torch.bfloat16)
     st = TrieState(R, b, t_max, cap, L, Hq, Hkv, D, V, prompts, lens, window=W,
-                   dtype=torch.bfloat16)
+                   dtype=torch.bfloat16, n_pages=R * cap // 64 if paged else 0)
     path = _lib.trie_attn_plan_info(st.cfg, b, 0)["path"]
     assert path in paths, f"{name}: planned path {path}"
     kp, vp = st.new_pools()
-    logits = gm.prefill(prompts, lens, kp, vp, window=W)
+    if paged:  # prefill into dense rows, then through the page table
+        kd = torch.zeros(L, R, Hkv, cap, D, dtype=torch.bfloat16, device="cuda")
+        vd = torch.zeros_like(kd)
+        logits = gm.prefill(prompts, lens, kd, vd, window=W)
+        for l in range(L):
+            st.write_rows(kp[l], kd[l][:, :, :t_max])
+            st.write_rows(vp[l], vd[l][:, :, :t_max])
+    else:
+        logits = gm.prefill(prompts, lens, kp, vp, window=W)
+    dense = lambda pool: st.dense_view(pool)  # noqa: E731  slot-order rows (paged or not)
     # the oracle's tries, carrying the K/V rows (as bf16 values in float64) per slot
     tries = [Trie([int(x) for x in prompts[r][: lens[r]]], n_layers=L) for r in range(R)]
     for r, T in enumerate(tries):
         for l in range(L):
-            K, Vv = _bf16_np(kp[l][r]), _bf16_np(vp[l][r])
+            K, Vv = _bf16_np(dense(kp[l])[r]), _bf16_np(dense(vp[l])[r])
             T.kv[l] = [(K[:, n], Vv[:, n]) for n in range(T.t)]
     checked_rows = 0
     for k in range(1, s + 1):
@@ -93,9 +107,11 @@ def test_bf16_lockstep_decode(name, D, Hq, Hkv, b, R, t_max, s, W, paths):
             assert tok[r, : T.N].tolist() == T.token and par[r, : T.N].tolist() == T.parent
             assert dep[r, : T.N].tolist() == T.depth and leaf[r].tolist() == T.leaves
         # the K/V rows the pools hold for every slot with K/V (pending leaves excluded)
+        KD = [_bf16_np(dense(kp[l])) for l in range(L)]
+        VD = [_bf16_np(dense(vp[l])) for l in range(L)]
         for r, T in enumerate(tries):
             for l in range(L):
-                K, Vv = _bf16_np(kp[l][r]), _bf16_np(vp[l][r])
+                K, Vv = KD[l][r], VD[l][r]
                 for n in range(T.N):
                     if T.kv[l][n] is not None:
                         assert np.array_equal(K[:, n], T.kv[l][n][0]) and \
@@ -106,7 +122,7 @@ def test_bf16_lockstep_decode(name, D, Hq, Hkv, b, R, t_max, s, W, paths):
         rec = {}
 
         def hook(l, q, kk, vv, o):
-            rec[l] = tuple(_bf16_np(x) for x in (q, kk, vv, o)) + (_bf16_np(kp[l]), _bf16_np(vp[l]))
+            rec[l] = tuple(_bf16_np(x) for x in (q, kk, vv, o)) + (_bf16_np(dense(kp[l])), _bf16_np(dense(vp[l])))
         logits = gm.step(st, kp, vp, fused=True, hook=hook)
         torch.cuda.synchronize()
         for l in range(L):

@@ -32,21 +32,48 @@ CASES = [
 ]
 
 
+PAGED_CASES = [CASES[0], CASES[2], CASES[4], CASES[5], CASES[7]]
+
+
+def _check_pages(st, N, R, tag):
+    """Paged pools (NEXT-2): request r maps exactly blocks [0, ceil(N_r / 64)); the mapped
+    pages are distinct across requests; the prompt keeps its fixed pages; the device
+    in-use count equals the mapped pages."""
+    pt = st.page_table.cpu().numpy()
+    seen = []
+    for r in range(R):
+        nb = (int(N[r]) + 63) // 64
+        assert np.all(pt[r, :nb] >= 0) and np.all(pt[r, nb:] == -1), f"{tag} r {r}: mapped blocks"
+        pp = st.prompt_pages(r)
+        assert pt[r, : len(pp)].tolist() == pp, f"{tag} r {r}: prompt pages moved"
+        seen += pt[r, :nb].tolist()
+    assert len(seen) == len(set(seen)) and max(seen) < st.n_pages, f"{tag}: a page mapped twice"
+    ps = st.page_stats()
+    assert ps["in_use"] == len(seen) and ps["peak"] >= len(seen), f"{tag}: {ps} vs {len(seen)}"
+
+
+@pytest.mark.parametrize("paged", [False, True], ids=["dense", "paged"])
 @pytest.mark.parametrize("R,b,t_max,ragged,steps,rho,g", CASES)
-def test_append_prune_bit_exact(R, b, t_max, ragged, steps, rho, g):
+def test_append_prune_bit_exact(R, b, t_max, ragged, steps, rho, g, paged):
     need_gpu()
     from paper_2502_00085_b200.trie import TrieState
+    if paged and (R, b, t_max, ragged, steps, rho, g) not in PAGED_CASES:
+        pytest.skip("paged pools: a subset of the cases")
     seed = R * 100 + b
     V = 1000
     lens = synth.ragged_lens(seed, R, t_max) if ragged else None
     prompts, lens = synth.prompts(seed, R, t_max, V, lens)
     sels = per_request_selections(seed, R, steps, b, V, rho)
     cap = t_max + b * steps + b
+    if paged:  # NEXT-2: 64-slot pages; enough for the no-GC worst case of every request
+        cap = (cap + 63) // 64 * 64
     L, Hkv, D = 2, 2, 16
-    st = TrieState(R, b, t_max, cap, L, 2 * Hkv, Hkv, D, V, prompts, lens, dtype=torch.float32)
+    st = TrieState(R, b, t_max, cap, L, 2 * Hkv, Hkv, D, V, prompts, lens, dtype=torch.float32,
+                   n_pages=R * cap // 64 if paged else 0)
     kp, vp = st.new_pools()
 
     def write_kv(slots_per_req):
+        pt = st.page_table.cpu().numpy() if paged else None
         for r, slots in enumerate(slots_per_req):
             for n in slots:
                 dep, tok = int(st.depth[r, n]), int(st.token[r, n])
@@ -54,8 +81,12 @@ def test_append_prune_bit_exact(R, b, t_max, ragged, steps, rho, g):
                     for h in range(Hkv):
                         for kind, pool in ((0, kp), (1, vp)):
                             a, bb = _ident(dep, tok, l, h, kind)
-                            pool[l, r, h, n, 0] = a
-                            pool[l, r, h, n, 1] = bb
+                            if paged:
+                                pool[l, int(pt[r, n // 64]), h, n % 64, 0] = a
+                                pool[l, int(pt[r, n // 64]), h, n % 64, 1] = bb
+                            else:
+                                pool[l, r, h, n, 0] = a
+                                pool[l, r, h, n, 1] = bb
 
     write_kv([range(int(lens[r])) for r in range(R)])  # prompt prefill
     for k, (par, tok) in enumerate(sels, 1):
@@ -66,6 +97,12 @@ def test_append_prune_bit_exact(R, b, t_max, ragged, steps, rho, g):
         ref = soa(build_tries(prompts, lens, sels[:k], b, g=g, final_gc=True, t_sched=t_max), cap, b)
         N = st.n_nodes.cpu().numpy()
         assert np.array_equal(N, ref["N"]), f"step {k}: N {N} vs {ref['N']}"
+        if paged:
+            _check_pages(st, N, R, f"step {k}")
+            kd = torch.stack([st.dense_view(kp[l]) for l in range(L)])
+            vd = torch.stack([st.dense_view(vp[l]) for l in range(L)])
+        else:
+            kd, vd = kp, vp
         tokg, parg, depg = st.token.cpu().numpy(), st.parent.cpu().numpy(), st.depth.cpu().numpy()
         maskg = st.beam_mask.cpu().numpy().view(np.uint32)
         leafg = st.leaf.cpu().numpy()[:, :b]
@@ -79,8 +116,8 @@ def test_append_prune_bit_exact(R, b, t_max, ragged, steps, rho, g):
             # leaves are the last b slots and share depth t + k - 1 (invariant 2)
             assert np.array_equal(leafg[r], np.arange(n - b, n))
             # KV identity of every slot that holds K/V (all but the pending leaves)
-            kpn = kp[:, r, :, : n - b, :2].cpu().numpy()
-            vpn = vp[:, r, :, : n - b, :2].cpu().numpy()
+            kpn = kd[:, r, :, : n - b, :2].cpu().numpy()
+            vpn = vd[:, r, :, : n - b, :2].cpu().numpy()
             for l in range(L):
                 for h in range(Hkv):
                     exp0 = ref["depth"][r, : n - b] * 1000.0 + ref["token"][r, : n - b]
@@ -114,3 +151,30 @@ def test_empty_prompt_rejected():
     from paper_2502_00085_b200.trie import TrieState
     with pytest.raises(TrieError):
         TrieState(2, 2, 4, 20, 0, 1, 1, 16, 50, np.zeros((2, 4), np.int32), [3, 0], dtype=torch.float32)
+
+
+def test_paged_pool_exhaustion_latches_and_gc_returns_pages():
+    """NEXT-2: with too few pages the append latches TRIE_ST_CAPACITY; with just enough,
+    pruning returns pages that later appends reuse (in-use never exceeds the pool)."""
+    need_gpu()
+    from paper_2502_00085_b200._lib import TRIE_ST_CAPACITY
+    from paper_2502_00085_b200.trie import TrieState
+    prompts, lens = synth.prompts(3, 2, 60, 50)
+    # 2 prompt pages + 1 free page: the second 64-slot block of both requests cannot map
+    st = TrieState(2, 4, 60, 256, 0, 1, 1, 16, 50, prompts, lens, dtype=torch.float32, n_pages=3)
+    par = torch.zeros(2, 4, dtype=torch.int32, device="cuda")
+    tok = torch.arange(4, dtype=torch.int32, device="cuda")[None].repeat(2, 1)
+    st.append(par, tok)  # N = 64: still the prompt pages
+    st.append(par, tok)  # N = 68: both need a second page, one is free
+    assert st.status() & TRIE_ST_CAPACITY
+    # convergent chain (every new beam continues beam 0): GC keeps t + k + b - 1 rows, so
+    # the pages in use stay bounded while 40 steps append 160 rows per request
+    st2 = TrieState(1, 4, 60, 256, 0, 1, 1, 16, 50, prompts[:1], lens[:1], dtype=torch.float32, n_pages=3)
+    for k in range(40):
+        st2.append(par[:1], (tok[:1] + 4 * k) % 50)
+        st2.prune_compact([], [])
+    assert st2.status() == 0
+    N = int(st2.n_nodes[0])
+    assert N == 60 + 40 + 3
+    ps = st2.page_stats()
+    assert ps["in_use"] == (N + 63) // 64 and ps["peak"] <= 3
