@@ -430,6 +430,14 @@ class HotPath:
         torch.cuda.synchronize()
         g = self.attn_graph
         g.replay()
+        if os.environ.get("BENCH_PROFILE_REGION_C"):
+            # ncu --profile-from-start off: exactly one replay of region C's launches (the
+            # roofline's trie state) is profiled (scripts/ncu_region_c.sh)
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
+            g.replay()
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
         done = None
         if self.wl.get("eos_frac"):  # NEXT-3: requests whose beams all finished are skipped
             done = (self.st.finished.cpu().numpy()[:, :self.b] != 0).all(axis=1)

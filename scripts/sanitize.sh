@@ -20,8 +20,13 @@ IDS=(
   "$T/test_gpu_attn.py::test_rope_kv_append_matches_oracle"
   "$T/test_gpu_beam_step.py::test_beam_step_matches_oracle[2-3-256-4.0]"
   "$T/test_gpu_beam_step.py::test_beam_step_matches_oracle[2-16-4097-5.0]"
-  "$T/test_gpu_integer_path.py::test_append_prune_bit_exact[3-3-8-False-16-0.5-1]"
-  "$T/test_gpu_integer_path.py::test_append_prune_bit_exact[3-4-12-True-30-0.0-3]"
+  "$T/test_gpu_integer_path.py::test_append_prune_bit_exact[3-3-8-False-16-0.5-1-dense]"
+  "$T/test_gpu_integer_path.py::test_append_prune_bit_exact[3-4-12-True-30-0.0-3-dense]"
+  "$T/test_gpu_integer_path.py::test_append_prune_bit_exact[3-3-8-False-16-0.5-1-paged]"   # NEXT-2 pages
+  "$T/test_gpu_integer_path.py::test_paged_pool_exhaustion_latches_and_gc_returns_pages"
+  "$T/test_gpu_attn.py::test_fused_paged_pools_match_oracle[paged-wide-2-8-150-32-8-128-0]"
+  "$T/test_gpu_attn.py::test_fused_paged_pools_match_oracle[paged-umma-2-16-400-8-2-128-0]"
+  "$T/test_gpu_attn.py::test_swa_eviction_frees_prompt_pages_and_matches_oracle[evict-narrow-2-4-300-8-2-128-100-8]"
   "$T/test_gpu_batch_baseline.py::test_batch_reorder_matches_gather"
 )
 for tool in memcheck racecheck synccheck initcheck; do
