@@ -646,12 +646,12 @@ static const UKernel* select_u(int D, bool rope = false) {
   return nullptr;
 }
 
-// tcgen05 path for Qg in [umma_min_qg, 128]; TRIE_UMMA_MIN_QG overrides (0 disables)
-// Which query groups take the tcgen05 kernel.  Default (measured r20, D = 128): every
-// Qg >= 33 (mma.sync is tensor-pipe bound there), and Qg >= 9 when a request holds
-// >= 1024 rows (sweep t = 8192: Qg = 16 6.22 vs 5.97 TB/s narrow, Qg = 32 6.10 vs 5.95
-// wide; Mistral shard Qg = 16: 16.5 vs 19.2 us) -- its fixed per-CTA cost (TMEM
-// allocation, barrier setup) loses on short tries (Llama t = 150: 26.8 vs 14.2 us).
+// Which query groups take the tcgen05 kernel: Qg >= 33 (mma.sync is tensor-pipe bound
+// there).  Round 1 also sent Qg >= 9 with >= 1024 rows per request here (measured at job
+// steps 5-35); on the mid-job window (r2r, round 2) the mma.sync kernels with split-K over
+// all 148 SMs are faster per launch -- sweep b = 4 (Qg 16) 101.2 vs 104.8 us, b = 8 (Qg
+// 32) 103.0 vs 114.2 us, Mistral shard (Qg 16) 60.4 vs 63.4 us -- while the tcgen05 grid
+// of R x Hkv = 128 one-CTA-per-SM items leaves 20 SMs idle.
 // TRIE_UMMA_MIN_QG = n overrides with the plain rule Qg >= n (0 disables).
 int attn_umma_min_qg() {
   static int v = -2;
@@ -666,7 +666,7 @@ bool attn_umma_eligible(const AttnParams& p) {
   if (Qg > 128 || !attn_tc_shape_ok(p)) return false;
   const int mn = attn_umma_min_qg();
   if (mn >= 0) return mn > 0 && Qg >= mn;
-  return Qg >= 33 || (Qg >= 9 && p.D == 128 && p.rows_hint >= 1024);
+  return Qg >= 33;
 }
 int attn_umma_occ(const AttnParams& p) {
   const UKernel* k = select_u(p.D);

@@ -56,7 +56,9 @@ def main():
         torch.cuda.synchronize()
     assert fn(buf, n) == 0
     t = np.frombuffer(buf, dtype=np.uint64).reshape(n, 8).astype(np.int64)
-    t = t[(t[:, 0] != 0) & (t[:, 4] != 0)]  # CTAs that ran an item (idle ones exit early)
+    keep = (t[:, 0] != 0) & (t[:, 4] != 0)  # CTAs that ran an item (idle ones exit early)
+    cta_id = np.nonzero(keep)[0]
+    t = t[keep]
     n = len(t)
     t0 = t[:, 0].min()
     names = ["start", "setup", "first_tile", "last_tile", "epilogue", "producer_done"]
@@ -77,6 +79,27 @@ def main():
           "| per-tile p50 us", np.median(dur["tiles"] / np.maximum(ntl - 1, 1)))
     sm = t[:, 6]
     print("CTAs per SM: max", np.bincount(sm).max(), "SMs used", len(np.unique(sm)))
+    # per-SM load: tiles of the SM's CTAs vs when its last CTA finished; CTA -> SM placement
+    sms = np.unique(sm)
+    load = np.array([ntl[sm == x].sum() for x in sms])
+    fin = np.array([rel["epilogue"][sm == x].max() for x in sms])
+    cnt = np.array([(sm == x).sum() for x in sms])
+    print("per-SM tiles: min", load.min(), "median", np.median(load), "max", load.max(),
+          "| corr(tiles, finish)", round(float(np.corrcoef(load, fin)[0, 1]), 3))
+    for c in (1, 2, 3, 4):
+        if (cnt == c).any():
+            print(f"  SMs with {c} CTA(s): {int((cnt == c).sum())}, tiles median {np.median(load[cnt == c]):.1f},"
+                  f" finish median {np.median(fin[cnt == c]):.2f} us")
+    gaps = [int(np.diff(np.sort(cta_id[sm == x]))[0]) for x in sms if (sm == x).sum() == 2]
+    if gaps:
+        u, c = np.unique(gaps, return_counts=True)
+        top = np.argsort(-c)[:5]
+        print("  CTA-index gap between the two CTAs of an SM (top):", [(int(u[i]), int(c[i])) for i in top])
+    per_tile = dur["tiles"] / np.maximum(ntl - 1, 1)
+    shared = np.array([cnt[np.searchsorted(sms, x)] for x in sm])
+    for c in (1, 2):
+        if (shared == c).any():
+            print(f"  per-tile us on SMs with {c} CTA(s): median {np.median(per_tile[shared == c]):.2f}")
     # occupancy over time: CTAs resident (start..epilogue) and streaming (first..last tile)
     end = rel["epilogue"].max()
     bins = np.linspace(0, end, 21)

@@ -233,8 +233,8 @@ def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False, steps=6, rho=0.5
 
 
 def test_attention_plan_paths():
-    """The kernel choice the bench relies on: narrow (Qg <= 16, short), wide (Qg 17..32,
-    short tries), tcgen05 (Qg >= 33, or Qg >= 9 at D = 128 with >= 1024 rows)."""
+    """The kernel choice the bench relies on: narrow (Qg <= 16), wide (Qg 17..32), tcgen05
+    (Qg >= 33) -- round 2: mma.sync with split-K also for long tries at Qg <= 32 (r2r)."""
     need_gpu()
     from paper_2502_00085_b200 import _lib
     import os
@@ -246,8 +246,9 @@ def test_attention_plan_paths():
         return _lib.trie_attn_plan_info(cfg, b, rows)["path"]
     assert path(4, 32, 32, 96, 1088, 864).startswith("narrow")         # Phi, Qg = 4
     assert path(8, 32, 8, 128, 448, 406).startswith("wide")            # Llama t=150, Qg = 32
-    assert path(8, 32, 8, 128, 8448, 8320).startswith("tcgen05")       # sweep t=8192, Qg = 32
-    assert path(4, 32, 8, 128, 8448, 8320).startswith("tcgen05")       # sweep, Qg = 16
+    assert path(8, 32, 8, 128, 8448, 8320).startswith("wide")          # sweep t=8192, Qg = 32
+    assert path(4, 32, 8, 128, 8448, 8320).startswith("narrow")        # sweep, Qg = 16
+    assert path(32, 32, 8, 128, 8448, 8320).startswith("tcgen05")      # sweep, Qg = 128
     assert path(16, 32, 8, 128, 448, 406).startswith("tcgen05")        # Qg = 64
     assert path(2, 32, 8, 128, 8448, 8320).startswith("narrow")        # Qg = 8
 
