@@ -1384,8 +1384,9 @@ def main():
                     help="NEXT-1 experiments: one whole instrumented job, per-step times and rows")
     ap.add_argument("--model-context", action="store_true",
                     help="also time the step inside a random-init model of the workload's shape")
-    ap.add_argument("--paged", type=float, default=0.0,
-                    help="NEXT-2: paged KV pools sized prompt + f x the no-GC generated pages")
+    ap.add_argument("--paged", type=float, default=0.5,
+                    help="NEXT-2: paged KV pools sized prompt + f x the no-GC generated pages "
+                         "(0: dense pools sized for the no-GC worst case)")
     ap.add_argument("--prompt-len", type=int, default=0)
     ap.add_argument("--new-tokens", type=int, default=0)
     ap.add_argument("--logit-scale", type=float, default=0.0,
