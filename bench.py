@@ -619,6 +619,9 @@ def run_batch(args):
     bp.k = 0
     for _ in range(args.warmup):
         bp.replay()
+    if args.steps < bp.s:  # the same mid-job window as the trie arm (run_gpu)
+        while bp.k != (bp.s - args.steps) // 2:
+            bp.replay()
     torch.cuda.synchronize()
     clocks = Clocks(0)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -649,6 +652,7 @@ def run_batch(args):
                                      "(generated rows; prompt rows not copied) into a second pool set"),
                kv_memory=dict(logical_bytes_mean=int(R * b * (t + k_mean) * kv_row),
                               physical_pool_bytes=int(bp.pool_bytes())),
+               execution=dict(timed_job_steps=[int(k_hist[0]), int(k_hist[-1])]),
                clocks=clk, gpu_launches=int(launches))
     return res
 

@@ -94,20 +94,22 @@ class TrieState:
                 m = min(64, n - blk * 64)
                 pool_l[int(pt[r, blk]), :, :m] = rows[r, :, blk * 64: blk * 64 + m]
 
-    def dense_view(self, pool_l, n=None):
-        """[R][Hkv][n][D] copy of a layer's pool in slot order (tests)."""
+    def dense_view(self, pool_l, n=None, requests=None):
+        """[R][Hkv][n][D] copy of a layer's pool in slot order (tests); `requests`: only those
+        (in that order)."""
         n = self.cap if n is None else n
+        reqs = list(range(self.R)) if requests is None else list(requests)
         if not self.n_pages:
-            return pool_l[:, :, :n].clone()
+            return pool_l[reqs, :, :n].clone()
         pt = self.page_table.cpu()
-        out = torch.zeros(self.R, self.Hkv, n, self.D, dtype=pool_l.dtype, device=pool_l.device)
-        for r in range(self.R):
+        out = torch.zeros(len(reqs), self.Hkv, n, self.D, dtype=pool_l.dtype, device=pool_l.device)
+        for i, r in enumerate(reqs):
             for blk in range((n + 63) // 64):
                 pg = int(pt[r, blk])
                 if pg < 0:
                     continue
                 m = min(64, n - blk * 64)
-                out[r, :, blk * 64: blk * 64 + m] = pool_l[pg, :, :m]
+                out[i, :, blk * 64: blk * 64 + m] = pool_l[pg, :, :m]
         return out
 
     def swa_evict(self, stream=None):

@@ -27,8 +27,11 @@ pytestmark = pytest.mark.gpu
 STEPS = 5
 
 
+@pytest.mark.parametrize("paged", [0.5, 0.0], ids=["paged", "dense"])
 @pytest.mark.parametrize("wl_name,beam", [("phi", 0), ("llama", 0), ("sweep", 16), ("mistral-shard", 0)])
-def test_fullsize_sampled_parity(wl_name, beam):
+def test_fullsize_sampled_parity(wl_name, beam, paged):
+    """paged = 0.5: bench.py's default pools (NEXT-2 pages: prompt + half the no-GC
+    generated pages); 0: dense pools sized for the no-GC worst case."""
     need_gpu()
     import bench
     from paper_2502_00085_b200 import _lib
@@ -38,6 +41,7 @@ def test_fullsize_sampled_parity(wl_name, beam):
     wl = dict(bench.WORKLOADS[wl_name])
     if beam:
         wl["b"] = beam
+    wl["paged"] = paged
     hp = bench.HotPath(wl, 0, torch.device("cuda", 0))
     st, R, b, t, V, L = hp.st, hp.R, hp.b, hp.t, hp.V, hp.L
     rs = sorted({0, R // 2, R - 1})
@@ -88,16 +92,18 @@ def test_fullsize_sampled_parity(wl_name, beam):
         o = out.float().cpu().numpy()
         for i, r in enumerate(rs):
             T = tries[i]
-            Kp = hp.kp[l][r, :, : T.N].float().cpu().numpy().astype(np.float64)
-            Vp = hp.vp[l][r, :, : T.N].float().cpu().numpy().astype(np.float64)
+            Kp = st.dense_view(hp.kp[l], T.N, [r])[0].float().cpu().numpy().astype(np.float64)
+            Vp = st.dense_view(hp.vp[l], T.N, [r])[0].float().cpu().numpy().astype(np.float64)
             qr = np.zeros_like(q0[r])
             for j, leaf in enumerate(T.leaves):
                 pos = int(T.depth[leaf])
                 for hh in range(q0.shape[2]):
                     qr[j, hh] = rope_rotate_half(q0[r, j, hh], pos, theta)
                 for hk in range(k0.shape[2]):  # the appended leaf rows (write-before-read)
-                    assert rel_err(Kp[hk, leaf], rope_rotate_half(k0[r, j, hk], pos, theta)) <= 1e-2
+                    krot = rope_rotate_half(k0[r, j, hk], pos, theta)
+                    assert rel_err(Kp[hk, leaf], krot) <= 1e-2
                     assert np.array_equal(Vp[hk, leaf], v0[r, j, hk])
+                    Kp[hk, leaf] = krot  # the reference attends over the oracle's own leaf rows
             o_ref, _ = attn_ref(qr, Kp, Vp, T, window=W)
             err = rel_err(o[r], o_ref)
             assert err <= 2e-2, f"{wl_name} layer {l} request {r}: rel err {err}"
