@@ -20,6 +20,18 @@
  *  - Threading: a handle is bound to one stream at a time and is not thread-safe;
  *    distinct handles are independent ("distinct sessions may run in
  *    parallel").
+ *  - CUDA graphs: all trie STATE (metadata, N, leaves, scores, tickets, page counters,
+ *    gather sequence numbers) lives on the device, so captured calls replay correctly at
+ *    any later step.  Two host-side quantities fix a call's LAUNCH SHAPE only: b_live
+ *    (1 until the first trie_beam_step / trie_append after trie_create / trie_reset, b
+ *    from then on) and, for trie_attn_decode_rope, whether the call recomputes the
+ *    (cos, sin) table of the leaves' depths (the first fused call after each beam step /
+ *    append does; the step counter `steps` is host-tracked for that).  Hence: capture
+ *    steady-state steps (b_live = b) as "beam step + the step's attention calls", and the
+ *    first step of a job (b_live = 1) as its own graph starting at trie_reset (bench.py's
+ *    "first" / "steady" graphs); do not replay a graph captured at b_live = 1 later in a
+ *    job, nor a graph holding only non-first fused attention calls of a step after a
+ *    beam step that was not replayed with it.
  *
  * DATA LAYOUT
  *  - KV pool, per layer: [R][Hkv][capacity][D], kv_dtype elements, head-major so that a

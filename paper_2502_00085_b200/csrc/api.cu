@@ -461,7 +461,7 @@ int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,
   const int Qg = b_live * (cfg->n_q_heads / cfg->n_kv_heads);
   int path = 0;
   if (trie::attn_tc_shape_ok(p))
-    path = trie::attn_umma_eligible(p) ? 3 : (Qg <= 16 ? 1 : 2);
+    path = trie::attn_umma_eligible(p) ? 3 : trie::attn_tc_variant(p);
   p.k = p.v = (const void*)(uintptr_t)256;  // aligned placeholders for the shape test
   const bool fused = trie::attn_rope_fusable(p);
   info_host[0] = path;

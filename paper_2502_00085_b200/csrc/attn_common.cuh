@@ -77,6 +77,7 @@ bool attn_tc_supported(const AttnParams& p);
 int launch_attn_combine_bf16(const AttnParams& p, cudaStream_t s);
 int attn_plan_splits(const AttnParams& p, int rows_est, int sms);
 bool attn_tc_shape_ok(const AttnParams& p);
+int attn_tc_variant(const AttnParams& p);  // 1 = narrow, 2 = wide (mma.sync kernels)
 bool attn_umma_eligible(const AttnParams& p);
 int attn_umma_occ(const AttnParams& p);
 int launch_attn_umma(const AttnParams& p, cudaStream_t s);

@@ -426,7 +426,10 @@ struct WideCfg {
 #ifdef TRIE_WIDE_STAGES  // experiment builds only
   static constexpr int STAGES = TRIE_WIDE_STAGES;
 #else
-  static constexpr int STAGES = D >= 128 ? 3 : 4;
+#ifndef TRIE_WIDE1_STAGES  // MT = 1 (8 < Qg <= 16) experiment builds only
+#define TRIE_WIDE1_STAGES 0
+#endif
+  static constexpr int STAGES = (MT == 1 && TRIE_WIDE1_STAGES > 0) ? TRIE_WIDE1_STAGES : (D >= 128 ? 3 : 4);
 #endif
   using RG = Ring<D, STAGES>;
   static constexpr int KS = D / 16;
@@ -436,8 +439,20 @@ struct WideCfg {
   static constexpr int NC = MT * RS;      // consumer warps
   static_assert(NT % 2 == 0, "row slice must be a multiple of 16");
   static_assert((RS - 1) * MT * 16 * (D + 2) * 4 <= RG::RING_BYTES, "merge buffer must fit the ring");
-  static constexpr int SMEM = RG::RING_BYTES + 2 * STAGES * 8 + 64 + 1024;
+  // RS >= 4: the rotated queries live in shared memory (fragment order, [MT][KS][32 lanes]
+  // x 16 B) instead of 32 registers per consumer thread, which is what lets 2 CTAs of 288
+  // threads share an SM under the 112-register cap below
+  static constexpr bool QS = RS >= 4;
+  static constexpr int OFF_Q = RG::RING_BYTES + 256;
+  static constexpr int Q_BYTES = QS ? MT * KS * 32 * 16 : 0;
+  static constexpr int SMEM = OFF_Q + Q_BYTES + 1024;
+  static_assert(2 * STAGES * 8 + 8 + (int)sizeof(ItemInfo) <= 256, "barrier area");
   static constexpr int THREADS = 32 * (NC + 1);
+  // Register cap: an SM sub-partition holds 16K registers and a CTA's warps are spread
+  // round-robin over the 4 sub-partitions, so 2 CTAs per SM need (warps on the fullest
+  // sub-partition) x 32 x regs <= 16384: 5 warps (MT = 2, RS = 4: 18 warps per SM) -> 96
+  // registers (Q staged in shared memory), 3 warps (two CTAs of 5 warps) -> 168
+  static constexpr int MAXREG = (MT == 2 && RS >= 4) ? 96 : 168;
 };
 
 // Warp (mt, rs) owns query m-tile mt (16 queries) and rows [rs*RSZ, (rs+1)*RSZ) of every
@@ -447,7 +462,7 @@ struct WideCfg {
 // (the rotate-half partner of column c < D/2 is column c + D/2, held by the same thread
 // in k-step ks + KS/2), the leaves' K/V rows are appended by the producer warp's idle lanes.
 template <int D, int MT, int RS, bool ROPE = false>
-__global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
+__global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) __maxnreg__((WideCfg<D, MT, RS>::MAXREG)) k_attn_wide(
     const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
     const AttnParams p, const __grid_constant__ CUtensorMap kmh,
     const __grid_constant__ CUtensorMap vmh) {
@@ -535,8 +550,10 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     if (p.window > 0 && qm[u] < Qg)
       lod[u] = p.depth[mbase + p.leaf[r * TRIE_MAX_BEAMS + beam[u]]] - p.window + 1;
   }
-  uint32_t qa[C::KS][4];
-  {
+  uint32_t qa[C::QS ? 1 : C::KS][4];
+  uint4* sq = (uint4*)(smem + C::OFF_Q) + (size_t)mt * C::KS * 32 + lane;  // QS: [ks * 32]
+  if (!C::QS || rs == 0) {
+    uint32_t ql[C::KS][4];  // rotated query fragments (QS: staged to shared memory)
     // the two query rows' base pointers (query m = beam j * g + head i of the group)
     const __nv_bfloat16* qrow[2];
 #pragma unroll
@@ -550,7 +567,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
       for (int u = 0; u < 4; ++u) {
         const __nv_bfloat16* src = qrow[u & 1];
         const int col = ks * 16 + (u >> 1) * 8 + cq * 2;
-        qa[ks][u] = src ? *(const uint32_t*)(src + col) : 0u;
+        ql[ks][u] = src ? *(const uint32_t*)(src + col) : 0u;
       }
     if constexpr (ROPE) {  // rotate-half at the beam's depth, rounded to bf16 like a-1
       constexpr int HALF = D / 2;
@@ -562,11 +579,20 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
           const int col = ks * 16 + (u >> 1) * 8 + cq * 2;  // < HALF; partner col + HALF
           const float4 t = __ldg((const float4*)(p.rope_tab +
                                                  ((size_t)r * p.b_live + beam[u & 1]) * HALF + col));
-          const float2 x1 = __bfloat1622float2(*(const __nv_bfloat162*)&qa[ks][u]);
-          const float2 x2 = __bfloat1622float2(*(const __nv_bfloat162*)&qa[ks + C::KS / 2][u]);
-          qa[ks][u] = pack_bf16(x1.x * t.x - x2.x * t.y, x1.y * t.z - x2.y * t.w);
-          qa[ks + C::KS / 2][u] = pack_bf16(x2.x * t.x + x1.x * t.y, x2.y * t.z + x1.y * t.w);
+          const float2 x1 = __bfloat1622float2(*(const __nv_bfloat162*)&ql[ks][u]);
+          const float2 x2 = __bfloat1622float2(*(const __nv_bfloat162*)&ql[ks + C::KS / 2][u]);
+          ql[ks][u] = pack_bf16(x1.x * t.x - x2.x * t.y, x1.y * t.z - x2.y * t.w);
+          ql[ks + C::KS / 2][u] = pack_bf16(x2.x * t.x + x1.x * t.y, x2.y * t.z + x1.y * t.w);
         }
+    }
+    if constexpr (C::QS) {
+#pragma unroll
+      for (int ks = 0; ks < C::KS; ++ks) sq[ks * 32] = make_uint4(ql[ks][0], ql[ks][1], ql[ks][2], ql[ks][3]);
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < C::KS; ++ks)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) qa[C::QS ? 0 : ks][u] = ql[ks][u];
     }
   }
   // item setup published by warp 0 (the queries were loaded and rotated meanwhile: r34 A/B
@@ -596,13 +622,20 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) k_attn_wide(
     for (int ks = 0; ks < C::KS; ++ks)
 #pragma unroll
       for (int nt = 0; nt < C::NT; nt += 2) {
+        if constexpr (C::QS) {
+          if (nt == 0) {
+            const uint4 q4 = sq[ks * 32];
+            qa[0][0] = q4.x; qa[0][1] = q4.y; qa[0][2] = q4.z; qa[0][3] = q4.w;
+          }
+        }
+        const int qk = C::QS ? 0 : ks;
         // x4: (n-tile nt, k lo), (nt, k hi), (nt+1, k lo), (nt+1, k hi)
         const int row = r0 + (nt + (lane >> 4)) * 8 + (lane & 7);
         const int col = ks * 16 + ((lane >> 3) & 1) * 8;
         uint32_t b0, b1, b2, b3;
         ldsm_x4(kbase + tile_off(row, col), b0, b1, b2, b3);
-        mma_bf16(sacc[nt], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-        mma_bf16(sacc[nt + 1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+        mma_bf16(sacc[nt], qa[qk][0], qa[qk][1], qa[qk][2], qa[qk][3], b0, b1);
+        mma_bf16(sacc[nt + 1], qa[qk][0], qa[qk][1], qa[qk][2], qa[qk][3], b2, b3);
       }
     float tmax[2] = {-INFINITY, -INFINITY};
     if (fast) {
@@ -914,8 +947,22 @@ static const TcKernel& narrow_sel() {
     default: return narrow_k<D, NQ, 2, ROPE>();
   }
 }
+// One query m-tile (Qg <= 16) over 4 row slices of the wide kernel (4 consumer warps of
+// 16 queries x 16 rows) beats the one-warp narrow kernel from Qg = 9 (r2z3, one B200:
+// Mistral shard Qg = 16 59.7 -> 55.3 us per launch, sweep b = 4 100.3 -> 96.1 us); knob
+// TRIE_WIDE1_MIN_QG = q (experiments): the wide kernel for q < Qg <= 16 (16 = never)
+static int wide1_min_qg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TRIE_WIDE1_MIN_QG");
+    v = e ? atoi(e) : 8;
+    if (v < 0 || v > 16) v = 8;
+  }
+  return v;
+}
 template <int D>
 static const TcKernel& select_d(int Qg, bool rope) {
+  if (Qg <= 16 && Qg > wide1_min_qg()) return rope ? wide_k<D, 1, 4, true>() : wide_k<D, 1, 4, false>();
   if (Qg <= 8) return rope ? narrow_sel<D, 1, true>() : narrow_sel<D, 1, false>();
   if (Qg <= 16) return rope ? narrow_sel<D, 2, true>() : narrow_sel<D, 2, false>();
   if (Qg <= 32) return rope ? wide_sel<D, 2, true>() : wide_sel<D, 2, false>();
@@ -929,6 +976,12 @@ static const TcKernel* select_tc(int D, int Qg, bool rope = false) {
     case 128: return &select_d<128>(Qg, rope);
   }
   return nullptr;
+}
+
+// mma.sync kernel family for a tensor-core shape: 1 = narrow, 2 = wide (plan reporting)
+int attn_tc_variant(const AttnParams& p) {
+  const int Qg = p.b_live * (p.Hq / p.Hkv);
+  return (Qg <= 16 && Qg > wide1_min_qg()) || Qg > 16 ? 2 : 1;
 }
 
 // The fused RoPE + append variants: narrow (Qg <= 16), wide at Qg <= 32, tcgen05.

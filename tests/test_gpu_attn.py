@@ -151,6 +151,8 @@ def test_swa_eviction_frees_prompt_pages_and_matches_oracle(name, R, b, t_max, H
     ("wide-fused", 1, 8, 130, 8, 2, 128, 0),      # Qg = 32: wide kernel, fused
     ("wide-fused-llama", 2, 8, 150, 32, 8, 128, 0),
     ("wide-fused-split", 1, 6, 1000, 16, 4, 64, 0),  # Qg = 24, D = 64, split K
+    ("wide1-fused-split", 1, 4, 1500, 8, 2, 64, 0),  # Qg = 16: one m-tile, 4 row slices, split K
+    ("wide1-fused-q12", 2, 3, 300, 8, 2, 96, 0),     # Qg = 12: padded query rows
     ("umma-fused", 1, 16, 130, 8, 2, 128, 0),     # Qg = 64: tcgen05, fused
     ("umma-fused-swa", 2, 16, 400, 8, 2, 128, 100),
     ("umma-fused-d96", 1, 12, 300, 8, 2, 96, 0),  # Qg = 48
@@ -166,6 +168,7 @@ def test_fused_rope_attention_matches_oracle(name, R, b, t_max, Hq, Hkv, D, W):
     ("wide-ragged", 6, 8, 1500, 32, 8, 128),   # Llama shape, requests of 1-24 tiles
     ("wide-ragged-many", 40, 8, 700, 8, 2, 128),
     ("wide-ragged-d96", 3, 6, 900, 12, 3, 96),  # Qg = 24, D = 96
+    ("wide1-ragged", 6, 4, 1500, 32, 8, 128),  # Mistral-like Qg = 16, requests of 1-24 tiles
 ])
 def test_fused_ragged_matches_oracle(name, R, b, t_max, Hq, Hkv, D):
     """Fused RoPE + wide attention on requests of very different lengths, vs the oracle."""
@@ -233,8 +236,9 @@ def _fused_case(name, R, b, t_max, Hq, Hkv, D, W, ragged=False, steps=6, rho=0.5
 
 
 def test_attention_plan_paths():
-    """The kernel choice the bench relies on: narrow (Qg <= 16), wide (Qg 17..32), tcgen05
-    (Qg >= 33) -- round 2: mma.sync with split-K also for long tries at Qg <= 32 (r2r)."""
+    """The kernel choice the bench relies on: narrow (Qg <= 8), wide (Qg 9..32; one query
+    m-tile over 4 row slices for Qg <= 16, r2z3), tcgen05 (Qg >= 33) -- round 2: mma.sync
+    with split-K also for long tries at Qg <= 32 (r2r)."""
     need_gpu()
     from paper_2502_00085_b200 import _lib
     import os
@@ -247,7 +251,8 @@ def test_attention_plan_paths():
     assert path(4, 32, 32, 96, 1088, 864).startswith("narrow")         # Phi, Qg = 4
     assert path(8, 32, 8, 128, 448, 406).startswith("wide")            # Llama t=150, Qg = 32
     assert path(8, 32, 8, 128, 8448, 8320).startswith("wide")          # sweep t=8192, Qg = 32
-    assert path(4, 32, 8, 128, 8448, 8320).startswith("narrow")        # sweep, Qg = 16
+    assert path(4, 32, 8, 128, 8448, 8320).startswith("wide")          # sweep, Qg = 16 (r2z3)
+    assert path(4, 32, 8, 128, 4224, 4100).startswith("wide")          # Mistral shard, Qg = 16
     assert path(32, 32, 8, 128, 8448, 8320).startswith("tcgen05")      # sweep, Qg = 128
     assert path(16, 32, 8, 128, 448, 406).startswith("tcgen05")        # Qg = 64
     assert path(2, 32, 8, 128, 8448, 8320).startswith("narrow")        # Qg = 8

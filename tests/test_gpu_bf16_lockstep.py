@@ -32,7 +32,9 @@ pytestmark = pytest.mark.gpu
 # name, D, Hq, Hkv, b, R, t_max, s, W, expected attention path (trie_attn_plan_info)
 CASES = [
     ("narrow-mha", 64, 4, 4, 4, 3, 150, 18, 0, ("narrow-mma.sync",)),
-    ("narrow-gqa", 64, 8, 2, 4, 3, 140, 17, 0, ("narrow-mma.sync",)),
+    ("narrow-gqa", 64, 8, 2, 2, 3, 140, 17, 0, ("narrow-mma.sync",)),
+    ("wide1-gqa", 128, 8, 2, 4, 3, 150, 17, 0, ("wide-mma.sync",)),   # Qg = 16: one m-tile
+    ("wide1-swa", 96, 8, 4, 8, 2, 130, 17, 100, ("wide-mma.sync",)),   # Qg = 16, D = 96
     ("wide", 128, 8, 2, 8, 3, 150, 17, 0, ("wide-mma.sync",)),
     ("wide-swa", 128, 8, 2, 8, 2, 130, 17, 100, ("wide-mma.sync",)),
     ("tcgen05", 128, 8, 1, 8, 2, 150, 17, 0, ("tcgen05-tmem",)),
@@ -49,7 +51,7 @@ def test_bf16_lockstep_decode(name, D, Hq, Hkv, b, R, t_max, s, W, paths, paged)
     """paged: the same decode over paged pools (pages mapped as the
     trie grows, returned by GC)."""
     need_gpu()
-    if paged and name not in ("narrow-gqa", "wide-swa", "tcgen05"):
+    if paged and name not in ("narrow-gqa", "wide-swa", "wide1-gqa", "tcgen05"):
         pytest.skip("paged pools: a subset of the shapes")
     from paper_2502_00085_b200 import _lib
     from paper_2502_00085_b200.model import TinyModel
