@@ -169,9 +169,9 @@ __global__ void __launch_bounds__(PRUNE_BS) k_prune_scan(
 // ---- §3.5 Compaction of the KV cache (the paper's index_select) -----------------
 // One CTA per (request, layer, group of hg KV heads): the K and V rows of the moved slots
 // of those heads (regions no other CTA touches), 16-byte vectors, (source, destination)
-// pairs written by k_prune_scan so a copy is two dependent loads deep.  hg keeps the grid
-// near 4096 CTAs (r61: one head per CTA cut Llama's GC 40 -> 25 us per step but made Phi's
-// 32-head launch of 65k CTAs slower, 44 -> 78 us).  Moves are applied in ascending
+// pairs written by k_prune_scan.  hg keeps the grid near 2048 CTAs of 256 threads (r61:
+// one head per CTA cut Llama's GC 40 -> 25 us per step but made Phi's 32-head launch of
+// 65k CTAs slower, 44 -> 78 us).  Moves are applied in ascending
 // batches (read-all, barrier, write-all) for the same in-place safety argument as above;
 // a few moved rows per request (r08 ncu: ~9 on Llama) fit one batch.
 struct PoolPtrs {
@@ -179,14 +179,19 @@ struct PoolPtrs {
   void* v[TRIE_MAX_LAYERS];
 };
 
-constexpr int COMPACT_BS = 128;
-constexpr int COMPACT_VEC = 4;  // 16-byte vectors in flight per thread per batch
+constexpr int COMPACT_BS = 256;
+constexpr int COMPACT_VEC = 8;   // 16-byte vectors in flight per thread per batch
+constexpr int COMPACT_MV = 512;  // (source, destination) pairs staged in shared memory per pass
+// The request's move list is staged in shared memory once per CTA (one coalesced read per
+// COMPACT_MV pairs), so a batch is ONE dependent global load deep (the K/V vectors) before
+// its stores, with up to 256 x 8 x 16 B = 32 KB in flight per CTA.
 __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant__ PoolPtrs pp,
                                                            const int32_t* moves,
                                                            const int32_t* moves_dst,
                                                            const int32_t* n_moves, int Hkv,
                                                            int hg, int row_bytes, int cap,
                                                            const int32_t* __restrict__ pt) {
+  __shared__ int sm_src[COMPACT_MV], sm_dst[COMPACT_MV];
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x, layer = blockIdx.y, h0 = blockIdx.z * hg;
@@ -199,42 +204,50 @@ __global__ void __launch_bounds__(COMPACT_BS) k_kv_compact(const __grid_constant
   const size_t hstride = (size_t)cap * row_bytes;
   char* kb = (char*)pp.k[layer] + hoff;
   char* vb = (char*)pp.v[layer] + hoff;
-  const int per_batch = COMPACT_BS * COMPACT_VEC;
+  const int* ptr = pt ? pt + r * (cap / 64) : nullptr;
   const int per_slot = 2 * nh * vpr;
-  const long total = (long)nm * per_slot;
-  for (long b0 = 0; b0 < total; b0 += per_batch) {
-    int4 val[COMPACT_VEC];
-    char* dstp[COMPACT_VEC];
-#pragma unroll
-    for (int u = 0; u < COMPACT_VEC; ++u) {
-      const long e = b0 + (long)u * COMPACT_BS + threadIdx.x;
-      dstp[u] = nullptr;
-      if (e < total) {
-        const int mi = (int)(e / per_slot);
-        int rem = (int)(e % per_slot);
-        const int kv = rem / (nh * vpr);
-        rem -= kv * nh * vpr;
-        const int hh = rem / vpr, c = rem % vpr;
-        const int src = moves[base + mi], dst = moves_dst[base + mi];
-        if (pt) {  // paged pools (NEXT-2): rows (page * Hkv + h) * 64 + slot % 64
-          char* pool = (char*)(kv ? pp.v[layer] : pp.k[layer]);
-          const int* ptr = pt + r * (cap / 64);
-          const size_t rs = ((size_t)ptr[src >> 6] * Hkv + h0 + hh) * 64 + (src & 63);
-          const size_t rd = ((size_t)ptr[dst >> 6] * Hkv + h0 + hh) * 64 + (dst & 63);
-          val[u] = *(const int4*)(pool + rs * row_bytes + (size_t)c * 16);
-          dstp[u] = pool + rd * row_bytes + (size_t)c * 16;
-          continue;
-        }
-        char* pool = (kv ? vb : kb) + (size_t)hh * hstride;
-        val[u] = *(const int4*)(pool + (size_t)src * row_bytes + (size_t)c * 16);
-        dstp[u] = pool + (size_t)dst * row_bytes + (size_t)c * 16;
-      }
+  for (int m0 = 0; m0 < nm; m0 += COMPACT_MV) {
+    const int cnt = min(COMPACT_MV, nm - m0);
+    __syncthreads();  // the previous pass's reads of sm_src / sm_dst are done
+    for (int i = threadIdx.x; i < cnt; i += COMPACT_BS) {
+      sm_src[i] = moves[base + m0 + i];
+      sm_dst[i] = moves_dst[base + m0 + i];
     }
     __syncthreads();
+    const int total = cnt * per_slot;
+    for (int b0 = 0; b0 < total; b0 += COMPACT_BS * COMPACT_VEC) {
+      int4 val[COMPACT_VEC];
+      char* dstp[COMPACT_VEC];
 #pragma unroll
-    for (int u = 0; u < COMPACT_VEC; ++u)
-      if (dstp[u]) *(int4*)dstp[u] = val[u];
-    __syncthreads();
+      for (int u = 0; u < COMPACT_VEC; ++u) {
+        const int e = b0 + u * COMPACT_BS + threadIdx.x;
+        dstp[u] = nullptr;
+        if (e < total) {
+          const int mi = e / per_slot;
+          int rem = e - mi * per_slot;
+          const int kv = rem / (nh * vpr);
+          rem -= kv * nh * vpr;
+          const int hh = rem / vpr, c = rem - hh * vpr;
+          const int src = sm_src[mi], dst = sm_dst[mi];
+          if (ptr) {  // paged pools (NEXT-2): rows (page * Hkv + h) * 64 + slot % 64
+            char* pool = (char*)(kv ? pp.v[layer] : pp.k[layer]);
+            const size_t rs = ((size_t)ptr[src >> 6] * Hkv + h0 + hh) * 64 + (src & 63);
+            const size_t rd = ((size_t)ptr[dst >> 6] * Hkv + h0 + hh) * 64 + (dst & 63);
+            val[u] = *(const int4*)(pool + rs * row_bytes + (size_t)c * 16);
+            dstp[u] = pool + rd * row_bytes + (size_t)c * 16;
+            continue;
+          }
+          char* pool = (kv ? vb : kb) + (size_t)hh * hstride;
+          val[u] = *(const int4*)(pool + (size_t)src * row_bytes + (size_t)c * 16);
+          dstp[u] = pool + (size_t)dst * row_bytes + (size_t)c * 16;
+        }
+      }
+      __syncthreads();  // in-place safety: every read of the batch before any write
+#pragma unroll
+      for (int u = 0; u < COMPACT_VEC; ++u)
+        if (dstp[u]) *(int4*)dstp[u] = val[u];
+      __syncthreads();
+    }
   }
 }
 
@@ -311,7 +324,7 @@ int launch_prune(trie_handle* h, void* const* kp, void* const* vp, cudaStream_t 
   }
   const int esz = c.kv_dtype == TRIE_BF16 ? 2 : 4;
   const long units = (long)c.n_requests * c.n_layers * c.n_kv_heads;
-  int hg = (int)((units + 4095) / 4096);
+  int hg = (int)((units + 2047) / 2048);
   if (hg > c.n_kv_heads) hg = c.n_kv_heads;
   if (hg < 1) hg = 1;
   dim3 grid(c.n_requests, c.n_layers, (c.n_kv_heads + hg - 1) / hg);
