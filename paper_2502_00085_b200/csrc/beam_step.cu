@@ -72,6 +72,7 @@ constexpr int ITEMS = 32;            // logits per thread
 constexpr int CHUNK = BS * ITEMS;    // 8192 logits per CTA
 static_assert(CHUNK == TRIE_BEAM_CHUNK, "workspace sizing (handle.h)");
 constexpr int CAND_CAP = 512;        // candidate keys buffered by the chunk stage
+constexpr int RANK_MAX = 128;        // row / request stage: rank counting up to this many keys
 
 // Descending top-k of n unique keys (0 = empty) by rank counting: out[rank(x)] = x for
 // rank < k, out[] zero-filled first.  Block-wide; src may be shared or global memory.
@@ -408,11 +409,14 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
   const size_t o = (size_t)row * a.chunks + c;
   uint64_t* ctop = a.chunk_top + o * a.b;
   const int n_cand = sm_n;
-  if (n_cand <= 32) {  // common case: one warp sorts the candidates
+  if (n_cand <= 32) {  // common case: one warp ranks the candidates (unique keys) by
+    // counting larger ones with broadcast shared-memory reads -- no dependent shuffle chain
     if (w == 0) {
-      uint64_t key = lane < n_cand ? sm_cand[lane] : 0ull;
-      key = warp_sort_desc_u64(key);
-      if (lane < k) ctop[lane] = key;
+      const uint64_t key = lane < n_cand ? sm_cand[lane] : 0ull;
+      int rank = 0;
+      for (int j = 0; j < n_cand; ++j) rank += sm_cand[j] > key ? 1 : 0;
+      if (lane < n_cand && rank < k) ctop[rank] = key;
+      if (lane >= n_cand && lane < k) ctop[lane] = 0ull;  // fewer than k candidates
     }
   } else if (n_cand <= CAND_CAP) {
     block_rank_topk(sm_cand, n_cand, k, ctop);
@@ -478,8 +482,16 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
   }
   // the chunk lists (sorted descending, zero padded) merged: each warp folds chunks
   // w, w + 8, ... into a running top-32, then a 3-level tree over the warps
+  // (up to RANK_MAX keys: staged in shared memory and ranked by counting, one key per
+  // thread, instead of the 3-level merge tree's dependent shuffle / barrier chain; r2s5:
+  // Phi 18.2 -> 17.4 us, but 256 / 512 keys (b = 16 / 32) are slower than the tree)
   const uint64_t* lists = a.chunk_top + rowi * a.b;
-  {
+  if (a.chunks * k <= RANK_MAX) {
+    const int n = a.chunks * k;
+    for (int i = threadIdx.x; i < n; i += BS) sm_cand[i] = __ldcg(lists + (size_t)(i / k) * a.b + i % k);
+    __syncthreads();
+    block_rank_topk(sm_cand, n, k, sm_mrg[0]);
+  } else {
     uint64_t acc = 0ull;
     for (int cc = w; cc < a.chunks; cc += BS / 32) {
       const uint64_t x = lane < k ? __ldcg(lists + (size_t)cc * a.b + lane) : 0ull;
@@ -524,7 +536,23 @@ __device__ __forceinline__ void beam_item(const BeamStepArgs& a, int row, int c,
   // each warp takes rows w, w + 8, ...: lane = position in the row's list.  The row list
   // is in (x desc, v asc) order, which is (cs desc) order up to fp32 ties of cs; re-sort
   // only if a tie left it out of global-key order, then merge (as in the row stage)
-  {
+  if (b_live * k <= RANK_MAX) {  // all b_live x k global keys ranked by counting (as above)
+    const int n = b_live * k;
+    for (int i = threadIdx.x; i < n; i += BS) {
+      const int j = i / k;
+      uint64_t gk = 0ull;
+      const uint64_t rk = __ldcg(a.row_top + ((size_t)r * TRIE_MAX_BEAMS + j) * TRIE_MAX_BEAMS + i % k);
+      if (rk != 0ull) {
+        const float xv = ord2f((uint32_t)(rk >> 32));
+        const uint32_t v = ~(uint32_t)rk;
+        const float cs = a.score[r * TRIE_MAX_BEAMS + j] + (xv - sm_lse[j]);
+        gk = ((uint64_t)f2ord(cs) << 32) | (uint32_t)(~(v * (uint32_t)b_live + j));
+      }
+      sm_cand[i] = gk;
+    }
+    __syncthreads();
+    block_rank_topk(sm_cand, n, k, sm_mrg[0]);
+  } else {
     uint64_t acc = 0ull;
     for (int j = w; j < b_live; j += BS / 32) {
       uint64_t gk = 0ull;
