@@ -1,4 +1,5 @@
 #!/bin/bash
+# NOTE (r2f3): compute-sanitizer has been closed on the GPU pool; kept for the record of r2l.
 # compute-sanitizer (memcheck / racecheck / synccheck / initcheck) over every kernel of the
 # library at tiny shapes, through the GPU parity tests (SURVEY §5 / §4 tier vi).
 #   bash scripts/sanitize.sh <tag>   -> gpurun_out/<tag>_san_<tool>.log
@@ -17,6 +18,8 @@ IDS=(
   "$T/test_gpu_attn.py::test_fused_rope_attention_matches_oracle[wide-fused-llama-2-8-150-32-8-128-0]"
   "$T/test_gpu_attn.py::test_fused_rope_attention_matches_oracle[umma-fused-1-16-130-8-2-128-0]"
   "$T/test_gpu_attn.py::test_fused_rope_attention_matches_oracle[split-fused-1-2-1500-2-2-128-0]"
+  "$T/test_gpu_attn.py::test_fused_rope_attention_matches_oracle[gqa-fused-2-4-200-8-2-128-0]"          # wide<128,1,4> (Qg = 16)
+  "$T/test_gpu_attn.py::test_fused_rope_attention_matches_oracle[wide1-fused-split-1-4-1500-8-2-64-0]"  # wide<64,1,4> + split-K
   "$T/test_gpu_attn.py::test_rope_kv_append_matches_oracle"
   "$T/test_gpu_beam_step.py::test_beam_step_matches_oracle[2-3-256-4.0]"
   "$T/test_gpu_beam_step.py::test_beam_step_matches_oracle[2-16-4097-5.0]"
