@@ -442,7 +442,14 @@ struct WideCfg {
   // RS >= 4: the rotated queries live in shared memory (fragment order, [MT][KS][32 lanes]
   // x 16 B) instead of 32 registers per consumer thread, which is what lets 2 CTAs of 288
   // threads share an SM under the 112-register cap below
-  static constexpr bool QS = RS >= 4;
+#ifndef TRIE_WIDE_PIPE  // one-tile software pipeline of the consumer loop (A/B knob)
+#define TRIE_WIDE_PIPE 1
+#endif
+  // one-m-tile kernel only (r2p1, one box, A/B vs the plain loop): sweep b = 4 96.0 -> 91.0
+  // us per launch, Mistral shard 54.8 -> 54.0; at MT = 2 it was slower (Llama 27.5 -> 31.1
+  // us, sweep b = 8 102.6 -> 107.4) -- the isolated per-CTA tile time rises there too
+  static constexpr bool PIPE = TRIE_WIDE_PIPE != 0 && MT == 1;
+  static constexpr bool QS = RS >= 4 || (PIPE && MT >= 2);
   static constexpr int OFF_Q = RG::RING_BYTES + 256;
   static constexpr int Q_BYTES = QS ? MT * KS * 32 * 16 : 0;
   static constexpr int SMEM = OFF_Q + Q_BYTES + 1024;
@@ -606,16 +613,12 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) __maxnreg__((Wide
   const float sc = p.scale_log2;
   const int fast_end = min(it.t, it.N) / TC_TR;
 
-  for (int i = 0; i < it.ntiles; ++i) {
+  // S = Q K^T of tile i (this warp's rows) into sacc; waits for the tile's stage
+  auto qk_tile = [&](int i, float (&sacc)[C::NT][4]) {
     const int s = i % C::STAGES;
     mbar_wait(&full[s], (uint32_t)(i / C::STAGES) & 1u);
     ATTN_TRC(i == 0 && cw == 0 && lane == 0, 2);
-    const uint8_t* st = ring + s * RG::STAGE_BYTES;
-    const uint32_t kbase = smem_u32(st), vbase = smem_u32(st + RG::TILE_BYTES);
-    const int tile = it.tile0 + i;
-    const int n0 = tile * TC_TR;
-    const bool fast = tile >= it.fast_from && tile < fast_end;
-    float sacc[C::NT][4];
+    const uint32_t kbase = smem_u32(ring + s * RG::STAGE_BYTES);
 #pragma unroll
     for (int nt = 0; nt < C::NT; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
 #pragma unroll
@@ -637,6 +640,15 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) __maxnreg__((Wide
         mma_bf16(sacc[nt], qa[qk][0], qa[qk][1], qa[qk][2], qa[qk][3], b0, b1);
         mma_bf16(sacc[nt + 1], qa[qk][0], qa[qk][1], qa[qk][2], qa[qk][3], b2, b3);
       }
+  };
+  // mask + online softmax of tile i's scores, O += P V, release the stage
+  auto softmax_pv_tile = [&](int i, float (&sacc)[C::NT][4]) {
+    const int s = i % C::STAGES;
+    const uint8_t* st = ring + s * RG::STAGE_BYTES;
+    const uint32_t vbase = smem_u32(st + RG::TILE_BYTES);
+    const int tile = it.tile0 + i;
+    const int n0 = tile * TC_TR;
+    const bool fast = tile >= it.fast_from && tile < fast_end;
     float tmax[2] = {-INFINITY, -INFINITY};
     if (fast) {
 #pragma unroll
@@ -716,6 +728,25 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) __maxnreg__((Wide
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+  };
+  float sA[C::NT][4];
+  if constexpr (C::PIPE) {
+    // one-tile software pipeline: tile i+1's QK^T MMAs are issued ahead of tile i's
+    // softmax, so the tensor-pipe chains overlap the ALU / MUFU work of the same warp
+    float sB[C::NT][4];
+    if (it.ntiles > 0) qk_tile(0, sA);
+    for (int i = 0; i < it.ntiles; i += 2) {
+      if (i + 1 < it.ntiles) qk_tile(i + 1, sB);
+      softmax_pv_tile(i, sA);
+      if (i + 1 >= it.ntiles) break;
+      if (i + 2 < it.ntiles) qk_tile(i + 2, sA);
+      softmax_pv_tile(i + 1, sB);
+    }
+  } else {
+    for (int i = 0; i < it.ntiles; ++i) {
+      qk_tile(i, sA);
+      softmax_pv_tile(i, sA);
+    }
   }
   ATTN_TRC(cw == 0 && lane == 0, 3);
 #pragma unroll
