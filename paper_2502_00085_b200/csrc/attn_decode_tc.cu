@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
         for (int nq = 0; nq < NQ; ++nq)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float v = qok[nq][e & 1] ? sacc[mt][nq][e] * sc : -INFINITY;
+            const float v = qok[nq][e & 1] ? sacc[mt][nq][e] : -INFINITY;
             sacc[mt][nq][e] = v;
             tmax[nq][e & 1] = fmaxf(tmax[nq][e & 1], v);
           }
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const bool ok = (vis & bbit[nq][e]) != 0u && dep >= lod[nq][e];
-              const float v = ok ? sacc[mt][nq][hh * 2 + e] * sc : -INFINITY;
+              const float v = ok ? sacc[mt][nq][hh * 2 + e] : -INFINITY;
               sacc[mt][nq][hh * 2 + e] = v;
               tmax[nq][e] = fmaxf(tmax[nq][e], v);
             }
@@ -298,11 +298,16 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
         v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
         v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
         v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
-        const float mnew = fmaxf(mq[nq][e], v);
-        alpha[nq][e] = (mnew == -INFINITY) ? 1.f : exp2f(mq[nq][e] - mnew);
+        const float mnew = fmaxf(mq[nq][e], v * sc);  // scores are raw until here (sc > 0)
+        alpha[nq][e] = (mnew == -INFINITY) ? 1.f : ex2_ftz(mq[nq][e] - mnew);
         mq[nq][e] = mnew;
         lq[nq][e] *= alpha[nq][e];
       }
+    float msafe[NQ][2];
+#pragma unroll
+    for (int nq = 0; nq < NQ; ++nq)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) msafe[nq][e] = mq[nq][e] == -INFINITY ? 0.f : mq[nq][e];
     // ---- P^T -> B fragments of O^T = V^T P^T (movmatrix.trans) ----
     uint32_t pb[4][NQ][2];
 #pragma unroll
@@ -313,7 +318,9 @@ __global__ void __launch_bounds__(64) k_attn_narrow(const __grid_constant__ CUte
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float x = sacc[mt][nq][e];
-          pv[e] = (x == -INFINITY) ? 0.f : exp2f(x - mq[nq][e & 1]);
+          // -inf - m -> 2^-inf = 0 with one MUFU (m is finite once any key of the query was
+          // visible; before that every score is -inf and msafe = 0)
+          pv[e] = ex2_ftz(fmaf(x, sc, -msafe[nq][e & 1]));
           lq[nq][e & 1] += pv[e];
         }
         pb[mt][nq][0] = movm_t(pack_bf16(pv[0], pv[1]));  // rows gq      -> B rows 0..7
@@ -656,7 +663,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) __maxnreg__((Wide
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int u = e >> 1;
-          const float v = qm[u] < Qg ? sacc[nt][e] * sc : -INFINITY;
+          const float v = qm[u] < Qg ? sacc[nt][e] : -INFINITY;
           sacc[nt][e] = v;
           tmax[u] = fmaxf(tmax[u], v);
         }
@@ -664,34 +671,51 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) __maxnreg__((Wide
       const uint32_t* tmask = (const uint32_t*)(st + 2 * RG::TILE_BYTES);
       const int* tdep = (const int*)(st + 2 * RG::TILE_BYTES + TC_TR * 4);
       const bool win = p.window > 0;
+      if (!win && n0 >= it.t && n0 + TC_TR <= it.N) {
+        // generated rows only, all below N, no window: the beam word alone decides
 #pragma unroll
-      for (int nt = 0; nt < C::NT; ++nt)
+        for (int nt = 0; nt < C::NT; ++nt)
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int lr = r0 + nt * 8 + cq * 2 + cc;
-          const int n = n0 + lr;
-          // visible-beam word of the row: none past N, all on the prompt (Alg. 3 l.2)
-          const uint32_t vis = n >= it.N ? 0u : (n < it.t ? ~0u : tmask[lr]);
-          const int dep = win ? tdep[lr] : 0;
+          for (int cc = 0; cc < 2; ++cc) {
+            const uint32_t vis = tmask[r0 + nt * 8 + cq * 2 + cc];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const bool ok = (vis & bbit[u]) != 0u && dep >= lod[u];
-            const float v = ok ? sacc[nt][u * 2 + cc] * sc : -INFINITY;
-            sacc[nt][u * 2 + cc] = v;
-            tmax[u] = fmaxf(tmax[u], v);
+            for (int u = 0; u < 2; ++u) {
+              const float v = (vis & bbit[u]) != 0u ? sacc[nt][u * 2 + cc] : -INFINITY;
+              sacc[nt][u * 2 + cc] = v;
+              tmax[u] = fmaxf(tmax[u], v);
+            }
           }
-        }
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < C::NT; ++nt)
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int lr = r0 + nt * 8 + cq * 2 + cc;
+            const int n = n0 + lr;
+            // visible-beam word of the row: none past N, all on the prompt (Alg. 3 l.2)
+            const uint32_t vis = n >= it.N ? 0u : (n < it.t ? ~0u : tmask[lr]);
+            const int dep = win ? tdep[lr] : 0;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const bool ok = (vis & bbit[u]) != 0u && dep >= lod[u];
+              const float v = ok ? sacc[nt][u * 2 + cc] : -INFINITY;
+              sacc[nt][u * 2 + cc] = v;
+              tmax[u] = fmaxf(tmax[u], v);
+            }
+          }
+      }
     }
     float alpha[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 1));
       tmax[u] = fmaxf(tmax[u], __shfl_xor_sync(0xffffffffu, tmax[u], 2));
-      const float mnew = fmaxf(mrow[u], tmax[u]);
-      alpha[u] = (mnew == -INFINITY) ? 1.f : exp2f(mrow[u] - mnew);
+      const float mnew = fmaxf(mrow[u], tmax[u] * sc);  // scores are raw until here (sc > 0)
+      alpha[u] = (mnew == -INFINITY) ? 1.f : ex2_ftz(mrow[u] - mnew);
       mrow[u] = mnew;
       lrow[u] *= alpha[u];
     }
+    const float msafe[2] = {mrow[0] == -INFINITY ? 0.f : mrow[0], mrow[1] == -INFINITY ? 0.f : mrow[1]};
     uint32_t pa[C::NT][2];
 #pragma unroll
     for (int nt = 0; nt < C::NT; ++nt) {
@@ -699,7 +723,7 @@ __global__ void __launch_bounds__(WideCfg<D, MT, RS>::THREADS) __maxnreg__((Wide
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int u = e >> 1;
-        pv[e] = (sacc[nt][e] == -INFINITY) ? 0.f : exp2f(sacc[nt][e] - mrow[u]);
+        pv[e] = ex2_ftz(fmaf(sacc[nt][e], sc, -msafe[u]));  // masked keys: 2^-inf = 0
         lrow[u] += pv[e];
       }
       pa[nt][0] = pack_bf16(pv[0], pv[1]);

@@ -84,6 +84,18 @@ __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
+// 2^x by one MUFU.EX2 (ex2.approx.ftz: ~2 ulp, 2^-inf = +0, results below 2^-126 flushed to
+// zero -- softmax weights that small are below bf16 P's resolution anyway); exp2f adds a
+// denormal range fix-up (compare + two predicated multiplies) around the same MUFU
+__device__ __forceinline__ float ex2_ftz(float x) {
+#ifdef TRIE_EXP2_PRECISE  // A/B builds only: the libdevice exp2f
+  return exp2f(x);
+#else
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+#endif
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *(uint32_t*)&v;
