@@ -217,8 +217,9 @@ int trie_attn_plan_info(const trie_cfg* cfg, int32_t b_live, int32_t rows_hint,
                         int32_t* info_host);
 
 /*
- * a-1 + a-3 fused (one launch when the narrow tensor-core kernel applies: bf16, D in
- * {64, 96, 128}, b_live * Hq/Hkv <= 16): the same result as trie_rope_kv_append followed
+ * a-1 + a-3 fused (one launch when a tensor-core kernel applies: bf16, D in {64, 96, 128},
+ * Qg = b_live * Hq/Hkv <= 32 (narrow for Qg <= 8, wide above) or the tcgen05 kernel for
+ * Qg >= 33; trie_attn_plan_info [2]): the same result as trie_rope_kv_append followed
  * by trie_attn_decode over the handle's trie (window = cfg.window), except that q and
  * k_new are read un-rotated and not written back.  Each attention CTA rotates its own
  * query heads at the beams' depths and, if its tiles contain leaf slots, rotates and
