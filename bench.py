@@ -841,8 +841,10 @@ def run_gpu(args):
                                             beam_step=round(float(np.mean(beam_ms)), 4),
                                             gc=round(float(np.mean(gc_ms)), 4),
                                             step=round(ms_b / args.steps, 4),
-                                            note="region B event nodes; the model GEMMs are context "
-                                                 "and not in the step (SURVEY §8(d))"),
+                                            note="region B event nodes (they also break the PDL chain, "
+                                                 "so the short beam-step / gc intervals read high: "
+                                                 "scripts/gc_cost.py measures gc without them); the "
+                                                 "model GEMMs are context and not in the step (SURVEY §8(d))"),
                                         timing="CUDA event nodes around every attention launch of "
                                                f"{args.steps} instrumented step graphs "
                                                f"({ms_b / args.steps:.3f} ms/step; includes the "
